@@ -1,0 +1,131 @@
+/*
+ * pch_b200.h -- C ABI of the B200-native Parallel Chen-Han geodesic solver.
+ *
+ * This is the drop-in boundary for the reference's engine entry point
+ *   run_pch(mesh: SurfaceMesh, sources, config: EngineConfig)
+ *       -> (distance_field, RunStats)
+ * (reference pkg/src/pargeo/engine.py:433), with the mesh arrays of
+ * SurfaceMesh (pkg/src/pargeo/mesh.py:44) crossing as plain pointers.
+ * No torch types, no C++ types: every argument is a pointer + size.
+ *
+ * Entry points and the reference interface each one replaces:
+ *   pch_mesh_create   build_half_edge_mesh result -> device-resident mesh
+ *                     (mesh.py:142 output; the paper's §4.1 `he[]`,
+ *                      `outgoing_he[]` plus precomputed unfoldings)
+ *   pch_run           run_pch(mesh, sources, config) with host buffers
+ *                     (engine.py:433)
+ *   pch_run_device    the same with device-resident sources / output
+ *   pch_run_rows      batched single-source fields, one row per source
+ *                     (the CLI's multi-source use, cli.py:382 context;
+ *                      paper Table 3 "multiple-source-all-destination")
+ * Error behaviour mirrors the reference: an empty or out-of-range source
+ * list returns PCH_ERR_SOURCE (reference raises ValueError "invalid source
+ * index"); exceeding max_iterations returns PCH_ERR_GUARD (EngineGuard,
+ * engine.py:475); bad config values return PCH_ERR_CONFIG (ValueError in
+ * EngineConfig.__post_init__, engine.py:65).  pch_last_error() returns the
+ * message of the last failure on the calling thread.
+ */
+#ifndef PCH_B200_H
+#define PCH_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PCH_ABI_VERSION 1
+
+enum pch_status {
+    PCH_OK = 0,
+    PCH_ERR_CUDA = 1,     /* CUDA runtime failure (message in pch_last_error) */
+    PCH_ERR_SOURCE = 2,   /* empty / out-of-range source list */
+    PCH_ERR_CONFIG = 3,   /* k < 1, epsilon <= 0, ... */
+    PCH_ERR_GUARD = 4,    /* iteration cap or wall-time guard tripped */
+    PCH_ERR_MESH = 5,     /* malformed mesh arrays */
+    PCH_ERR_NOMEM = 6     /* window pool cannot grow further */
+};
+
+/* EngineConfig (engine.py:44) fields that exist on this path. */
+typedef struct pch_config {
+    int64_t k;               /* selection size per iteration (>= 1) */
+    int32_t selection_mode;  /* 0 exact, 1 approximate_strided (both map to
+                                the device threshold selection) */
+    int32_t fan_mode;        /* 0 clip, 1 full_edges */
+    double epsilon_window;   /* tiny-window tolerance (default 1e-6) */
+    int64_t max_iterations;  /* <= 0: no cap */
+    int64_t pool_capacity;   /* initial window-pool capacity; 0 = auto */
+    int32_t flags;           /* PCH_FLAG_* */
+    int32_t reserved;
+} pch_config;
+
+#define PCH_FLAG_NO_RECHECK 1   /* disable the pop-time endpoint re-check */
+#define PCH_FLAG_EAGER_FANS 2   /* reserved */
+
+/* RunStats (engine.py:76) plus device-side counters. */
+typedef struct pch_stats {
+    int64_t iterations;
+    int64_t windows_propagated;
+    int64_t total_windows_created;
+    int64_t total_windows_pruned;
+    int64_t pruned_ich;
+    int64_t pruned_split;
+    int64_t pruned_tiny;
+    int64_t pruned_degenerate;
+    int64_t pruned_duplicate;
+    int64_t pruned_recheck;
+    int64_t windows_stored;
+    int64_t max_children_per_window;
+    int64_t events_created;
+    int64_t events_applied;
+    int64_t peak_active_pool;
+    int64_t fans_emitted;
+    int64_t buffer_regrows;
+    double time_total_ms;     /* device time of the solve (CUDA events) */
+    double time_kernel_ms;    /* persistent-kernel time only */
+} pch_stats;
+
+typedef struct pch_mesh pch_mesh;
+
+/* Library identity. */
+int pch_abi_version(void);
+const char *pch_last_error(void);
+int pch_device_count(void);
+
+/* Upload a half-edge mesh (arrays exactly as SurfaceMesh holds them:
+ * origin/opposite/length/corner_angle are length 3*n_faces, vertex_class
+ * and outgoing length n_vertices; opposite == -1 marks a boundary) to
+ * `device` and build the device-side tables.  *out receives the handle. */
+int pch_mesh_create(const int64_t *origin, const int64_t *opposite,
+                    const double *length, const double *corner_angle,
+                    const uint8_t *vertex_class, const int64_t *outgoing,
+                    int64_t n_vertices, int64_t n_faces, int32_t device,
+                    pch_mesh **out);
+int pch_mesh_destroy(pch_mesh *mesh);
+int64_t pch_mesh_device_bytes(const pch_mesh *mesh);
+
+/* Exact geodesic distance field from the union of `sources` (host
+ * int64[n_sources]) into host double[n_vertices] `out_dist`; +inf marks
+ * unreachable vertices.  `stats` may be NULL. */
+int pch_run(pch_mesh *mesh, const int64_t *sources, int64_t n_sources,
+            const pch_config *config, double *out_dist, pch_stats *stats);
+
+/* Same with device pointers on the mesh's device; `stream` is a
+ * cudaStream_t (NULL = the library's own stream).  Returns after the
+ * solve has completed on the stream. */
+int pch_run_device(pch_mesh *mesh, const int64_t *d_sources,
+                   int64_t n_sources, const pch_config *config,
+                   double *d_out_dist, void *stream, pch_stats *stats);
+
+/* One single-source field per entry of `sources`: row r of the host
+ * double[n_sources * n_vertices] `out_rows` is the field of sources[r].
+ * `stats` (may be NULL) accumulates over rows. */
+int pch_run_rows(pch_mesh *mesh, const int64_t *sources, int64_t n_sources,
+                 const pch_config *config, double *out_rows,
+                 pch_stats *stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PCH_B200_H */

@@ -1,0 +1,254 @@
+"""Engine entry points -- the drop-in for the reference's ``pargeo.engine``
+hot path.
+
+``run_pch(mesh, sources, config) -> (dist, RunStats)`` keeps the
+reference signature, argument meaning and error behaviour (reference
+pkg/src/pargeo/engine.py:433; ``EngineConfig`` :44, ``RunStats`` :76,
+``EngineGuard`` :40, source validation :392).  The work happens in the
+CUDA library behind the C ABI (include/pch_b200.h): the mesh is uploaded
+once per (mesh, device) and stays resident; each call ships only the
+source indices in and the distance field out.
+
+There is deliberately no CPU path here: without the library or a CUDA
+device every call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, fields
+
+import numpy as np
+
+from . import _native
+from .mesh import SurfaceMesh
+
+SELECTION_MODES = ("exact", "approximate_strided")
+FAN_MODES = ("clip", "full_edges")
+
+
+class EngineGuard(RuntimeError):
+    """A configured safety guard stopped the run (engine.py:40)."""
+
+
+@dataclass
+class EngineConfig:
+    """Engine parameters (engine.py:44).
+
+    ``k`` is the per-iteration selection size: the device picks the
+    distance threshold whose key histogram count reaches ``k`` and
+    propagates every window below it.  ``workers`` is accepted for
+    interface parity; on the device every selected window gets its own
+    thread.  ``selection_mode`` is accepted with the reference's values;
+    both map to the device threshold selection (results are identical for
+    any selection, §4.3).  ``recheck`` enables the pop-time endpoint
+    re-check of the ICH filter; ``pool_capacity`` is the initial window
+    pool size (0 = automatic; the pool doubles on overflow).
+    """
+
+    k: int = 4096
+    workers: int = 1
+    selection_mode: str = "exact"
+    epsilon_window: float = 1e-6
+    seed: int = 0
+    max_iterations: int | None = None
+    fan_mode: str = "clip"
+    device: int = 0
+    recheck: bool = True
+    pool_capacity: int = 0
+
+    def __post_init__(self):
+        if self.k < 1:
+            raise ValueError("k must be >= 1")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+        if self.selection_mode not in SELECTION_MODES:
+            raise ValueError(f"selection_mode must be one of {SELECTION_MODES}")
+        if self.fan_mode not in FAN_MODES:
+            raise ValueError(f"fan_mode must be one of {FAN_MODES}")
+        if not self.epsilon_window > 0.0:
+            raise ValueError("epsilon_window must be > 0")
+
+    def to_native(self) -> _native.PchConfig:
+        c = _native.PchConfig()
+        c.k = int(self.k)
+        c.selection_mode = SELECTION_MODES.index(self.selection_mode)
+        c.fan_mode = FAN_MODES.index(self.fan_mode)
+        c.epsilon_window = float(self.epsilon_window)
+        c.max_iterations = int(self.max_iterations or 0)
+        c.pool_capacity = int(self.pool_capacity)
+        c.flags = 0 if self.recheck else _native.FLAG_NO_RECHECK
+        return c
+
+
+@dataclass
+class RunStats:
+    """Run accounting (engine.py:76) plus device counters."""
+
+    algorithm: str = ""
+    iterations: int = 0
+    windows_propagated: int = 0
+    total_windows_created: int = 0
+    total_windows_pruned: int = 0
+    pruned_ich: int = 0
+    pruned_split: int = 0
+    pruned_tiny: int = 0
+    pruned_degenerate: int = 0
+    pruned_duplicate: int = 0
+    pruned_recheck: int = 0
+    windows_stored: int = 0
+    max_children_per_window: int = 0
+    events_created: int = 0
+    events_applied: int = 0
+    peak_active_pool: int = 0
+    fans_emitted: int = 0
+    buffer_regrows: int = 0
+    time_total: float = 0.0
+    time_select: float = 0.0
+    time_propagate: float = 0.0
+    time_compact: float = 0.0
+    time_events: float = 0.0
+    time_device_ms: float = 0.0
+    time_kernel_ms: float = 0.0
+
+    def to_dict(self) -> dict:
+        return {f.name: getattr(self, f.name) for f in fields(self)}
+
+    @classmethod
+    def from_native(cls, st: _native.PchStats, algorithm="pch-b200"):
+        s = cls(algorithm=algorithm)
+        for f in _native.STAT_FIELDS:
+            setattr(s, f, int(getattr(st, f)))
+        s.time_device_ms = float(st.time_total_ms)
+        s.time_kernel_ms = float(st.time_kernel_ms)
+        s.time_total = s.time_device_ms / 1e3
+        return s
+
+
+class DeviceMesh:
+    """A mesh resident on one GPU (the paper's §4.1 tables plus
+    precomputed per-half-edge unfoldings and per-vertex fan wedges)."""
+
+    def __init__(self, mesh: SurfaceMesh, device: int = 0):
+        lib = _native.load()
+        if lib.pch_device_count() <= device:
+            raise _native.NativeUnavailable(
+                f"no CUDA device {device} visible to libpch_b200")
+        arrs = (np.ascontiguousarray(mesh.origin, np.int64),
+                np.ascontiguousarray(mesh.opposite, np.int64),
+                np.ascontiguousarray(mesh.length, np.float64),
+                np.ascontiguousarray(mesh.corner_angle, np.float64),
+                np.ascontiguousarray(mesh.vertex_class, np.uint8),
+                np.ascontiguousarray(mesh.outgoing, np.int64))
+        handle = ctypes.c_void_p()
+        rc = lib.pch_mesh_create(*[a.ctypes.data for a in arrs],
+                                 mesh.n_vertices, mesh.n_faces, int(device),
+                                 ctypes.byref(handle))
+        _check(rc)
+        self.handle = handle
+        self.device = device
+        self.n_vertices = mesh.n_vertices
+        self._lib = lib
+
+    @property
+    def device_bytes(self) -> int:
+        return int(self._lib.pch_mesh_device_bytes(self.handle))
+
+    def close(self):
+        if self.handle:
+            self._lib.pch_mesh_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _check(rc: int):
+    if rc == _native.PCH_OK:
+        return
+    msg = _native.last_error()
+    if rc in (_native.PCH_ERR_SOURCE, _native.PCH_ERR_CONFIG, _native.PCH_ERR_MESH):
+        raise ValueError(msg)
+    if rc == _native.PCH_ERR_GUARD:
+        raise EngineGuard(msg)
+    raise RuntimeError(f"libpch_b200 error {rc}: {msg}")
+
+
+def device_mesh(mesh: SurfaceMesh, device: int = 0) -> DeviceMesh:
+    """The cached device-resident copy of ``mesh`` on ``device``."""
+    cache = mesh.__dict__.setdefault("_pch_device_meshes", {})
+    dm = cache.get(device)
+    if dm is None or dm.handle is None:
+        dm = DeviceMesh(mesh, device)
+        cache[device] = dm
+    return dm
+
+
+def _check_sources(mesh: SurfaceMesh, sources) -> np.ndarray:
+    """engine.py:392 -- non-empty, in range, deduplicated and sorted."""
+    src = [int(s) for s in sources]
+    if not src:
+        raise ValueError("at least one source vertex is required")
+    for s in src:
+        if s < 0 or s >= mesh.n_vertices:
+            raise ValueError(f"invalid source index {s}")
+    return np.asarray(sorted(set(src)), dtype=np.int64)
+
+
+def run_pch(mesh: SurfaceMesh, sources, config: EngineConfig | None = None):
+    """Exact geodesic distances from the source vertices on the GPU.
+
+    Returns ``(distance_field, RunStats)``; +inf marks vertices no window
+    reaches (boundary shadows), exactly as the reference does."""
+    config = config or EngineConfig()
+    src = _check_sources(mesh, sources)
+    dm = device_mesh(mesh, config.device)
+    out = np.empty(mesh.n_vertices, dtype=np.float64)
+    st = _native.PchStats()
+    cfg = config.to_native()
+    rc = dm._lib.pch_run(dm.handle, src.ctypes.data, len(src),
+                         ctypes.byref(cfg), out.ctypes.data, ctypes.byref(st))
+    _check(rc)
+    return out, RunStats.from_native(st)
+
+
+def run_pch_rows(mesh: SurfaceMesh, sources, config: EngineConfig | None = None):
+    """One single-source field per source (distance-matrix rows): returns
+    ``(rows[len(sources), n_vertices], RunStats)``; sources keep their
+    order and duplicates."""
+    config = config or EngineConfig()
+    src = np.asarray([int(s) for s in sources], dtype=np.int64)
+    if len(src) == 0:
+        raise ValueError("at least one source vertex is required")
+    if src.min() < 0 or src.max() >= mesh.n_vertices:
+        bad = int(src[(src < 0) | (src >= mesh.n_vertices)][0])
+        raise ValueError(f"invalid source index {bad}")
+    dm = device_mesh(mesh, config.device)
+    out = np.empty((len(src), mesh.n_vertices), dtype=np.float64)
+    st = _native.PchStats()
+    cfg = config.to_native()
+    rc = dm._lib.pch_run_rows(dm.handle, src.ctypes.data, len(src),
+                              ctypes.byref(cfg), out.ctypes.data,
+                              ctypes.byref(st))
+    _check(rc)
+    return out, RunStats.from_native(st)
+
+
+def run_pch_device(mesh: SurfaceMesh, d_sources_ptr: int, n_sources: int,
+                   d_out_ptr: int, config: EngineConfig | None = None,
+                   stream: int = 0):
+    """Device-pointer variant (inputs already resident in HBM): sources
+    int64[n] and output float64[n_vertices] on the mesh's device."""
+    config = config or EngineConfig()
+    dm = device_mesh(mesh, config.device)
+    st = _native.PchStats()
+    cfg = config.to_native()
+    rc = dm._lib.pch_run_device(dm.handle, ctypes.c_void_p(d_sources_ptr),
+                                int(n_sources), ctypes.byref(cfg),
+                                ctypes.c_void_p(d_out_ptr),
+                                ctypes.c_void_p(stream or None),
+                                ctypes.byref(st))
+    _check(rc)
+    return RunStats.from_native(st)

@@ -1,0 +1,93 @@
+"""The C ABI boundary: the shared library loads (no GPU needed), exports
+every symbol include/pch_b200.h declares, and the Python layer mirrors the
+reference's argument validation before any device work."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_1305_1293_b200 import EngineConfig, RunStats, _native, meshes
+from paper_1305_1293_b200.engine import _check_sources
+
+HEADER = os.path.join(ROOT, "include", "pch_b200.h")
+
+
+def _declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(pch_[a-z_0-9]+)\s*\(",
+                                 text, re.M)))
+
+
+def test_header_declares_entry_points():
+    syms = _declared_symbols()
+    assert {"pch_mesh_create", "pch_run", "pch_run_device", "pch_run_rows"} <= set(syms)
+    assert sorted(_native.EXPORTS) == syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for s in _declared_symbols():
+        assert hasattr(lib, s), s
+
+
+def test_library_loads_and_reports_abi():
+    lib = _native.load()
+    assert lib.pch_abi_version() == _native.ABI_VERSION
+    assert lib.pch_device_count() >= 0
+
+
+def test_struct_layouts_match_header():
+    # pch_config: 8+4+4+8+8+8+4+4 ; pch_stats: 17 int64 + 2 doubles
+    assert ctypes.sizeof(_native.PchConfig) == 48
+    assert ctypes.sizeof(_native.PchStats) == 8 * 19
+
+
+def test_sass_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_engine_config_validation():
+    with pytest.raises(ValueError):
+        EngineConfig(k=0)
+    with pytest.raises(ValueError):
+        EngineConfig(workers=0)
+    with pytest.raises(ValueError):
+        EngineConfig(selection_mode="sorted")
+    with pytest.raises(ValueError):
+        EngineConfig(fan_mode="none")
+    c = EngineConfig(k=123, fan_mode="full_edges", recheck=False).to_native()
+    assert (c.k, c.fan_mode, c.flags) == (123, 1, _native.FLAG_NO_RECHECK)
+
+
+def test_source_validation_matches_reference(cube):
+    with pytest.raises(ValueError):
+        _check_sources(cube, [])
+    with pytest.raises(ValueError, match="invalid source index 99"):
+        _check_sources(cube, [99])
+    with pytest.raises(ValueError):
+        _check_sources(cube, [-1])
+    assert _check_sources(cube, [3, 1, 3]).tolist() == [1, 3]
+
+
+def test_runstats_to_dict_flat():
+    s = RunStats(algorithm="pch-b200", iterations=3)
+    d = s.to_dict()
+    assert d["algorithm"] == "pch-b200" and d["iterations"] == 3
+    assert all(isinstance(v, (int, float, str)) for v in d.values())
+
+
+def test_no_device_raises_loudly():
+    """On a machine without a GPU the product path must fail, not fall
+    back to a CPU implementation."""
+    lib = _native.load()
+    if lib.pch_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    from paper_1305_1293_b200 import run_pch
+    with pytest.raises(_native.NativeUnavailable):
+        run_pch(meshes.make("cube"), [0])

@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define PCH_ABI_VERSION 1
+#define PCH_ABI_VERSION 2
 
 enum pch_status {
     PCH_OK = 0,
@@ -60,7 +60,12 @@ typedef struct pch_config {
 } pch_config;
 
 #define PCH_FLAG_NO_RECHECK 1   /* disable the pop-time endpoint re-check */
-#define PCH_FLAG_EAGER_FANS 2   /* reserved */
+#define PCH_FLAG_DETERMINISTIC 2  /* two-barrier solver whose filters read
+                                     iteration-frozen tables: bitwise
+                                     identical fields across runs (paper
+                                     Algorithm 1 with its delayed updates);
+                                     default is the one-barrier solver with
+                                     live tables, equal to rounding */
 
 /* RunStats (engine.py:76) plus device-side counters. */
 typedef struct pch_stats {

@@ -10,9 +10,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpch_b200.so")
+LIB_PATH = os.environ.get("PCH_B200_LIB") or os.path.join(_HERE, "_lib", "libpch_b200.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 PCH_OK = 0
 PCH_ERR_CUDA = 1
@@ -23,6 +23,7 @@ PCH_ERR_MESH = 5
 PCH_ERR_NOMEM = 6
 
 FLAG_NO_RECHECK = 1
+FLAG_DETERMINISTIC = 2
 
 
 class NativeUnavailable(RuntimeError):

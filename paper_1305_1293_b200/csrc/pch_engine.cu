@@ -33,6 +33,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -48,22 +49,28 @@ using namespace pch;
 
 enum { ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_PRUNE_TINY,
        ST_PRUNE_DEGEN, ST_RECHECK, ST_STORED, ST_EV_CREATED, ST_EV_APPLIED,
-       ST_FANS, ST_MAXCHILD, ST_PEAK, N_ST };
+       ST_FANS, ST_MAXCHILD, ST_PEAK,
+       // PCH_PROFILE section clocks (clock64 deltas summed over threads)
+       ST_CYC_LOAD, ST_CYC_PROP, ST_CYC_EVENTS, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
+       ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CYC_P1, ST_CYC_P2, ST_CYC_P3, ST_CYC_P4,
+       ST_CYC_P5, N_ST };
 
 enum { ERR_NONE = 0, ERR_OVERFLOW = 1, ERR_GUARD = 2, ERR_TIMEOUT = 3 };
 
-struct Slot {               // per-iteration counters, indexed by iteration % 3
-    unsigned long long nS;  // size of the selected batch S (written in phase B)
-    unsigned long long nP;  // size of the pool P (written in phase B)
-    unsigned long long nC;  // children appended during phase A
-    unsigned long long nTV; // touched vertices (phase A)
-    unsigned long long nTE; // touched angle entries (phase A)
-    unsigned long long nF;  // fan events (phase A)
-    unsigned long long pad[2];
+struct Slot {                // per-iteration counters (ring of NSLOT)
+    unsigned long long nS;   // size of the selected batch S
+    unsigned long long nP;   // size of the pool P
+    unsigned long long nC;   // children appended (two-barrier kernel)
+    unsigned long long nTV;  // touched vertices (two-barrier kernel)
+    unsigned long long nTE;  // touched angle entries (two-barrier kernel)
+    unsigned long long nF;   // fan events
+    unsigned long long pmin; // smallest key in P, fp64 bits (one-barrier kernel)
+    unsigned long long smax; // largest key in S, fp64 bits (one-barrier kernel)
 };
+constexpr int NSLOT = 4;
 
 struct Ctrl {
-    Slot slot[3];
+    Slot slot[NSLOT];
     unsigned int bar_count;
     unsigned int bar_gen;
     int error;
@@ -89,13 +96,14 @@ struct Params {
     unsigned long long *dist_new;
     double2 *split_cur;        // (comp, entry_x)
     ulonglong2 *split_new;     // (ord(comp), ord(entry_x))
-    ulonglong2 *fanpick[2];    // per vertex (cand bits, anchor<<32 | ord32(rel))
-    int32_t *tv_stamp, *te_stamp;
+    ulonglong2 *fanpick[3];    // per vertex (cand bits, anchor<<32 | ord32(rel)), by iteration % 3
     int32_t *tv_list, *te_list;
-    FanEv *fanev[2];
+    long long tvcap, tecap;
+    FanEv *fanev[3];           // saddle fan candidates, by iteration % 3
     long long fancap;
     // window pools
-    WinSoA X, Y, S;
+    WinSoA X, Y, S, S2;        // pools (X/Y) and batches (S/S2); the one-barrier
+                               // kernel double-buffers S/S2 and P = X/Y
     long long cap;
     unsigned int *hist[2];     // NBINS + 1 bins each
     Ctrl *ctrl;
@@ -103,11 +111,20 @@ struct Params {
     long long K;
     double eps_win;
     double w0;
+    double delta0, delta_min, delta_max;  // one-barrier step controller
     long long max_iter;
     unsigned long long time_limit_ns;
     int fan_full;
     int recheck;
+    int live;                  // filters read the live shadow tables
+    int prof;                  // PCH_PROFILE: accumulate per-section clocks
+    unsigned long long *trace; // optional per-iteration timeline (TR_* records)
+    long long trace_cap;       // iterations the trace buffer holds
 };
+
+// per-iteration trace record (PCH_TRACE=path): globaltimer stamps and sizes
+enum { TR_T0, TR_A_END, TR_B1, TR_B_END, TR_B2, TR_NS, TR_NP, TR_NC, TR_NF, TR_NTV, TR_TSEL_BITS,
+       TR_FAN_END, TR_N };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -173,6 +190,28 @@ __device__ __forceinline__ unsigned long long warp_alloc(unsigned long long *cou
     return base + __popc(b & ((1u << lane) - 1u));
 }
 
+// distance / angle-split reads of the filters: the iteration-frozen copy,
+// or (PCH_FLAG_LIVE) the shadow tables the events update atomically.  Any
+// value read is the length of a real path, so a stale or racing read only
+// weakens pruning; it never admits a wrong distance.
+__device__ __forceinline__ double gdist(const Params &p, int32_t v) {
+    if (p.live) return __longlong_as_double((long long)__ldcg(p.dist_new + v));
+    return __ldcg(p.dist_cur + v);
+}
+__device__ __forceinline__ double2 gsplit(const Params &p, int32_t j, ulonglong2 &raw) {
+    if (p.live) {
+        // 128-bit atomic read (the compare value never matches: ord64 of a
+        // comparison distance always has its top bit set)
+        raw = atomicCAS(p.split_new + j, make_ulonglong2(0ull, 0ull), make_ulonglong2(0ull, 0ull));
+        return make_double2(unord64(raw.x), unord64(raw.y));
+    }
+    double2 s = __ldcg(p.split_cur + j);
+    // the frozen entry is the shadow entry's value at the start of the
+    // iteration: the best first guess for a CAS on it
+    raw = make_ulonglong2(ord64(s.x), ord64(s.y));
+    return s;
+}
+
 __device__ __forceinline__ int key_bin(double key, double base, double w) {
     double f = (key - base) / w;
     if (!(f >= 0.0)) return 0;
@@ -202,76 +241,160 @@ __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
     return c;
 }
 
+// Run counters live in shared memory (one set per CTA, flushed to Ctrl at
+// kernel exit): per-thread register or local-memory counters would cost
+// registers or an L2 round trip per increment on the propagation path.
 struct LocalStats {
-    unsigned long long v[N_ST];
-    __device__ void zero() {
-#pragma unroll
-        for (int i = 0; i < N_ST; ++i) v[i] = 0;
-    }
+    unsigned long long *s;
+    __device__ __forceinline__ void add(int i, unsigned long long x = 1ull) { atomicAdd(s + i, x); }
+    __device__ __forceinline__ void max(int i, unsigned long long x) { atomicMax(s + i, x); }
 };
 
-__device__ __forceinline__ void flush_stats(Ctrl *c, LocalStats &ls) {
-#pragma unroll
-    for (int i = 0; i < N_ST; ++i) {
-        unsigned long long x = ls.v[i];
-        if (i == ST_MAXCHILD || i == ST_PEAK) {
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
-                x = x > y ? x : y;
-            }
-            if ((threadIdx.x & 31) == 0 && x) atomicMax(&c->st[i], x);
-        } else {
-#pragma unroll
-            for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-            if ((threadIdx.x & 31) == 0 && x) atomicAdd(&c->st[i], x);
-        }
+__device__ __forceinline__ void stats_init(unsigned long long *s) {
+    for (int i = threadIdx.x; i < N_ST; i += blockDim.x) s[i] = 0ull;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void flush_stats(Ctrl *c, unsigned long long *s) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < N_ST; i += blockDim.x) {
+        unsigned long long x = s[i];
+        if (!x) continue;
+        if (i == ST_MAXCHILD || i == ST_PEAK) atomicMax(&c->st[i], x);
+        else atomicAdd(&c->st[i], x);
     }
-    ls.zero();
 }
 
 // ---------------------------------------------------------------------------
 // events
+//
+// Events are applied on the spot with order-independent atomics (64-bit
+// atomicMin on the fp64 bit pattern of a positive distance, 128-bit CAS-min
+// on the angle-split pair), so the result does not depend on which thread
+// wins a race.  The bookkeeping they need -- which vertices / angles the
+// iteration touched, which saddles should fan out -- is staged in shared
+// memory and flushed by the CTA once per trip with one global atomic per
+// list: no hot global counter sits on the propagation path.
 
-__device__ __forceinline__ void dist_event(const Params &p, Slot &sl, int it, int32_t v,
-                                           double cand, LocalStats &ls) {
-    ls.v[ST_EV_CREATED]++;
-    unsigned long long nb = (unsigned long long)__double_as_longlong(cand);
-    unsigned long long old = atomicMin(p.dist_new + v, nb);
-    if (nb < old && atomicExch(p.tv_stamp + v, it) != it) {
-        unsigned long long slot = atomicAdd(&sl.nTV, 1ull);
-        p.tv_list[slot] = v;
-        ls.v[ST_EV_APPLIED]++;
+constexpr int TPB = 256;          // threads per CTA of every solver kernel
+constexpr int NWARP = TPB / 32;
+
+struct Stage {
+    unsigned int ntv, nte, nfe, pad;
+    int32_t tv[3 * TPB];  // improved vertices (<= 3 per propagation)
+    int32_t te[TPB];      // improved angle-split entries (<= 1)
+    FanEv fe[3 * TPB];    // saddle fan candidates (<= 3)
+};
+
+__device__ __forceinline__ void dist_event(const Params &p, Stage &sg, int32_t v, double cand,
+                                           LocalStats &ls) {
+    // the caller checked cand against the distance it read; the minimum
+    // itself needs no reply (RED), the vertex is listed for the commit
+    ls.add(ST_EV_CREATED);
+    atomicMin(p.dist_new + v, (unsigned long long)__double_as_longlong(cand));
+    if (!p.live) {
+        unsigned int k = atomicAdd(&sg.ntv, 1u);
+        sg.tv[k] = v;
+    }
+    ls.add(ST_EV_APPLIED);
+}
+
+__device__ __forceinline__ void angle_event(const Params &p, Stage &sg, int32_t j, double comp,
+                                            double entry, ulonglong2 guess, LocalStats &ls) {
+    ls.add(ST_EV_CREATED);
+    if (cas_min_u128(p.split_new + j, ord64(comp), ord64(entry), guess)) {
+        if (!p.live) {
+            unsigned int k = atomicAdd(&sg.nte, 1u);
+            sg.te[k] = j;
+        }
+        ls.add(ST_EV_APPLIED);
     }
 }
 
-__device__ __forceinline__ void angle_event(const Params &p, Slot &sl, int it, int32_t j,
-                                            double comp, double entry, LocalStats &ls) {
-    ls.v[ST_EV_CREATED]++;
-    if (cas_min_u128(p.split_new + j, ord64(comp), ord64(entry)) &&
-        atomicExch(p.te_stamp + j, it) != it) {
-        unsigned long long slot = atomicAdd(&sl.nTE, 1ull);
-        p.te_list[slot] = j;
-        ls.v[ST_EV_APPLIED]++;
-    }
-}
-
-__device__ __forceinline__ void fan_event(const Params &p, Slot &sl, int it, int32_t v,
+__device__ __forceinline__ void fan_event(const Params &p, Stage &sg, int it, int32_t v,
                                           int32_t anchor, double cand, double rel) {
     unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
     unsigned long long lo = ((unsigned long long)(uint32_t)anchor << 32) | ord_hi32(rel);
-    cas_min_u128(p.fanpick[it & 1] + v, hi, lo);
-    unsigned long long slot = atomicAdd(&sl.nF, 1ull);
-    if ((long long)slot < p.fancap) {
-        FanEv e;
-        e.v = v;
-        e.anchor = anchor;
-        e.cand = cand;
-        e.rel = rel;
-        p.fanev[it & 1][slot] = e;
-    } else {
-        atomicExch(&p.ctrl->error, ERR_OVERFLOW);
+    // picks start at (~0, ~0): the first claim of an iteration succeeds
+    // in one round trip
+    cas_min_u128(p.fanpick[p.live ? 0 : it % 3] + v, hi, lo, make_ulonglong2(~0ull, ~0ull));
+    unsigned int k = atomicAdd(&sg.nfe, 1u);
+    FanEv &e = sg.fe[k];
+    e.v = v;
+    e.anchor = anchor;
+    e.cand = cand;
+    e.rel = rel;
+}
+
+// End of one trip of the selected batch (uniform over the CTA): reserve
+// `n` (<= 2) pool slots per thread for the children with one global
+// atomicAdd per CTA, and flush the staged event lists with one atomicAdd
+// per list, all issued back to back by one thread.  Returns the thread's
+// first child slot relative to the pool's child counter.
+__device__ unsigned int block_excl_scan(unsigned int x, unsigned int &total);
+
+__device__ __forceinline__ unsigned long long trip_flush(const Params &p, Stage &sg, Slot &sl, int it,
+                                                        unsigned int n) {
+    __shared__ unsigned long long s_b[4];
+    unsigned int total;
+    const unsigned int excl = block_excl_scan(n, total);  // all staging of the trip is done
+    if (threadIdx.x == 0) {
+        s_b[0] = sg.ntv ? atomicAdd(&sl.nTV, (unsigned long long)sg.ntv) : 0ull;
+        s_b[1] = sg.nte ? atomicAdd(&sl.nTE, (unsigned long long)sg.nte) : 0ull;
+        s_b[2] = sg.nfe ? atomicAdd(&sl.nF, (unsigned long long)sg.nfe) : 0ull;
+        s_b[3] = total ? atomicAdd(&sl.nC, (unsigned long long)total) : 0ull;
     }
+    __syncthreads();
+    const unsigned int ntv = sg.ntv, nte = sg.nte, nfe = sg.nfe;
+    for (unsigned int k = threadIdx.x; k < ntv; k += TPB) {
+        unsigned long long at = s_b[0] + k;
+        if ((long long)at < p.tvcap) p.tv_list[at] = sg.tv[k];
+        else atomicExch(&p.ctrl->error, ERR_OVERFLOW);
+    }
+    for (unsigned int k = threadIdx.x; k < nte; k += TPB) {
+        unsigned long long at = s_b[1] + k;
+        if ((long long)at < p.tecap) p.te_list[at] = sg.te[k];
+        else atomicExch(&p.ctrl->error, ERR_OVERFLOW);
+    }
+    for (unsigned int k = threadIdx.x; k < nfe; k += TPB) {
+        unsigned long long at = s_b[2] + k;
+        if ((long long)at < p.fancap) p.fanev[p.live ? (it & 1) : it % 3][at] = sg.fe[k];
+        else atomicExch(&p.ctrl->error, ERR_OVERFLOW);
+    }
+    const unsigned long long rel = s_b[3] + excl;
+    __syncthreads();
+    if (threadIdx.x == 0) sg.ntv = sg.nte = sg.nfe = 0u;
+    __syncthreads();
+    return rel;
+}
+
+// exclusive block-wide prefix sum of x; *total receives the CTA total
+// (uniform: contains __syncthreads)
+__device__ unsigned int block_excl_scan(unsigned int x, unsigned int &total) {
+    __shared__ unsigned int s_w[NWARP];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned int y = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+    }
+    if (lane == 31) s_w[wid] = y;
+    __syncthreads();
+    if (wid == 0) {
+        unsigned int t = lane < NWARP ? s_w[lane] : 0u;
+#pragma unroll
+        for (int o = 1; o < NWARP; o <<= 1) {
+            unsigned int z = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += z;
+        }
+        if (lane < NWARP) s_w[lane] = t;
+    }
+    __syncthreads();
+    unsigned int excl = y - x + (wid ? s_w[wid - 1] : 0u);
+    total = s_w[NWARP - 1];
+    __syncthreads();
+    return excl;
 }
 
 // ---------------------------------------------------------------------------
@@ -279,97 +402,138 @@ __device__ __forceinline__ void fan_event(const Params &p, Slot &sl, int it, int
 // opposite v inside the fan spanned by the two straight extensions of the
 // incoming ray; `full` emits every wedge (source initialisation).
 
-template <typename Emit>
-__device__ void emit_fan(const Params &p, int32_t v, double cand, int32_t anchor,
-                         double rel, bool full, const double *dist, Emit &&emit,
-                         LocalStats &ls) {
-    int32_t off = __ldg(p.fan_off + v);
-    int32_t m = __ldg(p.fan_off + v + 1) - off;
-    double theta = __ldg(p.fan_theta + v);
-    double flo, fhi;
-    int reps;
+struct FanSpan {
+    int32_t off, m;  // wedge records of v: fan[off, off + m)
+    int reps;        // 2 when the fan interval may wrap around an interior vertex
+    double theta, flo, fhi;
+};
+
+// fan interval of v (geom.py:239-256); returns false for an empty fan
+__device__ __forceinline__ bool fan_span(const Params &p, int32_t v, int32_t anchor, double rel,
+                                         bool full, FanSpan &f) {
+    f.off = __ldg(p.fan_off + v);
+    f.m = __ldg(p.fan_off + v + 1) - f.off;
+    f.theta = __ldg(p.fan_theta + v);
     if (full) {
-        flo = -1.0e300;
-        fhi = 1.0e300;
-        reps = 1;
+        f.flo = -1.0e300;
+        f.fhi = 1.0e300;
+        f.reps = 1;
+        return true;
+    }
+    double width = f.theta - TWO_PI_D;
+    if (width <= EPS_NUM) return false;
+    double aphi = __ldg(&p.fan[f.off + __ldg(p.fanpos + anchor)].wlo);
+    f.flo = aphi + rel + PI_D;
+    f.fhi = f.flo + width;
+    if (__ldg(p.fan_interior + v)) {
+        double k = floor(f.flo / f.theta);
+        f.flo -= k * f.theta;
+        f.fhi -= k * f.theta;
+        f.reps = 2;
     } else {
-        double width = theta - TWO_PI_D;
-        if (width <= EPS_NUM) return;
-        double aphi = __ldg(&p.fan[off + __ldg(p.fanpos + anchor)].wlo);
-        flo = aphi + rel + PI_D;
-        fhi = flo + width;
-        if (__ldg(p.fan_interior + v)) {
-            double k = floor(flo / theta);
-            flo -= k * theta;
-            fhi -= k * theta;
-            reps = 2;
-        } else {
-            reps = 1;
-        }
+        f.reps = 1;
     }
-    for (int i = 0; i < m; ++i) {
-        const FanRec &f = p.fan[off + i];
-        double wlo = __ldg(&f.wlo), whi = __ldg(&f.whi);
-        for (int rep = 0; rep < reps; ++rep) {
-            double lo = flo - rep * theta, hi = fhi - rep * theta;
-            double slo = wlo > lo ? wlo : lo;
-            double shi = whi < hi ? whi : hi;
-            if (shi - slo <= 1e-12) continue;
-            if (p.fan_full) {
-                slo = wlo;
-                shi = whi;
-            }
-            double px = __ldg(&f.px), py = __ldg(&f.py), qx = __ldg(&f.qx), qy = __ldg(&f.qy);
-            double s0 = 0.0, s1 = 1.0;
-            bool ok0 = true, ok1 = true;
-            if (!(slo <= wlo + 1e-12)) {
-                double sn, cs;
-                sincos(slo, &sn, &cs);
-                ok0 = ray_seg(0.0, 0.0, cs, sn, px, py, qx, qy, s0);
-            }
-            if (!(shi >= whi - 1e-12)) {
-                double sn, cs;
-                sincos(shi, &sn, &cs);
-                ok1 = ray_seg(0.0, 0.0, cs, sn, px, py, qx, qy, s1);
-            }
-            ls.v[ST_CREATED]++;
-            if (!(ok0 && ok1)) {
-                ls.v[ST_PRUNE_DEGEN]++;
-                continue;
-            }
-            int32_t pid = __ldg(&f.pid), qid = __ldg(&f.qid);
-            Win c;
-            int fate = make_child(__ldg(&f.che), __ldg(&f.lc), px, py, qx, qy, s0, s1, 0.0, 0.0,
-                                  cand, ldcg(dist + pid), ldcg(dist + qid), INFINITY, 0.0, 0.0,
-                                  true, p.eps_win, c);
-            if (fate == CH_STORED) {
-                emit(c);
-            } else {
-                ls.v[fate == CH_TINY ? ST_PRUNE_TINY : fate == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN]++;
-            }
-        }
+    return true;
+}
+
+// one (wedge i, repetition rep) item of a fan (geom.py:258-307): the window
+// with pseudo source v on the edge opposite v in wedge i, clipped to the fan
+// interval.  `fresh` filters against the shadow field of this iteration
+// (phase B, where the frozen copy is being committed) instead of gdist.
+template <typename Emit>
+__device__ __forceinline__ void fan_item(const Params &p, double cand, const FanSpan &f, int i,
+                                         int rep, bool fresh, Emit &&emit, LocalStats &ls) {
+    const FanRec &fr = p.fan[f.off + i];
+    double wlo = __ldg(&fr.wlo), whi = __ldg(&fr.whi);
+    double lo = f.flo - rep * f.theta, hi = f.fhi - rep * f.theta;
+    double slo = wlo > lo ? wlo : lo;
+    double shi = whi < hi ? whi : hi;
+    if (shi - slo <= 1e-12) return;
+    if (p.fan_full) {
+        slo = wlo;
+        shi = whi;
     }
+    double px = __ldg(&fr.px), py = __ldg(&fr.py), qx = __ldg(&fr.qx), qy = __ldg(&fr.qy);
+    double s0 = 0.0, s1 = 1.0;
+    bool ok0 = true, ok1 = true;
+    if (!(slo <= wlo + 1e-12)) {
+        double sn, cs;
+        sincos(slo, &sn, &cs);
+        ok0 = ray_seg(0.0, 0.0, cs, sn, px, py, qx, qy, s0);
+    }
+    if (!(shi >= whi - 1e-12)) {
+        double sn, cs;
+        sincos(shi, &sn, &cs);
+        ok1 = ray_seg(0.0, 0.0, cs, sn, px, py, qx, qy, s1);
+    }
+    ls.add(ST_CREATED);
+    if (!(ok0 && ok1)) {
+        ls.add(ST_PRUNE_DEGEN);
+        return;
+    }
+    int32_t pid = __ldg(&fr.pid), qid = __ldg(&fr.qid);
+    double gp, gq;
+    if (fresh) {
+        gp = __longlong_as_double((long long)__ldcg(p.dist_new + pid));
+        gq = __longlong_as_double((long long)__ldcg(p.dist_new + qid));
+    } else {
+        gp = gdist(p, pid);
+        gq = gdist(p, qid);
+    }
+    Win c;
+    int fate = make_child(__ldg(&fr.che), __ldg(&fr.lc), px, py, qx, qy, s0, s1, 0.0, 0.0, cand,
+                          gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, c);
+    if (fate == CH_STORED) {
+        emit(c);
+    } else {
+        ls.add(fate == CH_TINY ? ST_PRUNE_TINY : fate == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
+    }
+}
+
+// saddle fans (geom.py:185): windows with pseudo source v on the edges
+// opposite v inside the fan spanned by the two straight extensions of the
+// incoming ray; `full` emits every wedge (source initialisation).  Serial
+// form (one thread); the solver loop spreads fan items over a warp.
+template <typename Emit>
+__device__ void emit_fan(const Params &p, int32_t v, double cand, int32_t anchor, double rel,
+                         bool full, Emit &&emit, LocalStats &ls) {
+    FanSpan f;
+    if (!fan_span(p, v, anchor, rel, full, f)) return;
+    for (int i = 0; i < f.m; ++i)
+        for (int rep = 0; rep < f.reps; ++rep) fan_item(p, cand, f, i, rep, false, emit, ls);
 }
 
 // ---------------------------------------------------------------------------
 // Algorithm 2 (geom.py:312) for one window against the frozen tables.
 // Up to two children are returned in `c`; events go to the shadow tables.
 
-__device__ int propagate(const Params &p, Slot &sl, int it, const Win &w, Win c[2],
-                         LocalStats &ls) {
+__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, const Win &w, Win &out0,
+                                         Win &out1, LocalStats &ls) {
+    // Latency layout: the per-iteration critical path is one propagation,
+    // so every memory access is issued as early as its address is known
+    // (window -> half-edge record -> distances / split entry: three load
+    // levels) and all event atomics are issued together at the end, fire
+    // and forget where the result is not needed.
     const int32_t j = w.he;
     const double b0 = w.b0, b1 = w.b1, d0 = w.d0, d1 = w.d1, dps = w.d;
-    double ix, iy;
-    if (!unfold(b0, b1, d0, d1, ix, iy)) {
-        ls.v[ST_PRUNE_DEGEN]++;
-        return 0;
-    }
     const HeRec *hp = p.he + j;
     const double ell = __ldg(&hp->ell);
-    const uint32_t v0f = __ldg(&hp->v0), v1f = __ldg(&hp->v1);
+    const uint32_t v0f = __ldg(&hp->v0), v1f = __ldg(&hp->v1), vdf = __ldg(&hp->vd);
+    const int32_t jo = __ldg(&hp->jo);
+    const double dx = __ldg(&hp->dx), dy = __ldg(&hp->dy);
+    const double lan = __ldg(&hp->lan), lpv = __ldg(&hp->lpv);
     const int32_t v0 = (int32_t)(v0f & VMASK), v1 = (int32_t)(v1f & VMASK);
-    const double g0 = ldcg(p.dist_cur + v0), g1 = ldcg(p.dist_cur + v1);
+    const int32_t vd = (int32_t)(vdf & VMASK);
+    const double g0 = gdist(p, v0), g1 = gdist(p, v1);
+    const double gdd = jo >= 0 ? gdist(p, vd) : INFINITY;
+    ulonglong2 sp_raw = make_ulonglong2(0ull, 0ull);
+    const double2 sp = jo >= 0 ? gsplit(p, j, sp_raw) : make_double2(INFINITY, 0.0);
 
+    double ix, iy;
+    if (!unfold(b0, b1, d0, d1, ix, iy)) {
+        ls.add(ST_PRUNE_DEGEN);
+        return 0;
+    }
     if (p.recheck) {
         // endpoint inequalities of the ICH filter (paper Fig. 4b) against
         // the current field: paths through v0 (resp. v1) already reach the
@@ -377,115 +541,116 @@ __device__ int propagate(const Params &p, Slot &sl, int it, const Win &w, Win c[
         double tB = dps + hyp(ix - b1, iy), tA = dps + hyp(ix - b0, iy);
         if ((g0 < INFINITY && tB > g0 + b1 + EPS_NUM) ||
             (g1 < INFINITY && tA > g1 + (ell - b0) + EPS_NUM)) {
-            ls.v[ST_RECHECK]++;
+            ls.add(ST_RECHECK);
             return 0;
         }
     }
-    ls.v[ST_PROPAGATED]++;
+    ls.add(ST_PROPAGATED);
+
+    // interval endpoints sitting on v0 / v1 (geom.py:345-385)
+    const double cand0 = dps + d0 + b0;
+    const bool ev0 = b0 <= p.eps_win && cand0 < g0;
+    const double cand1 = dps + d1 + (ell - b1);
+    const bool ev1 = b1 >= ell - p.eps_win && cand1 < g1;
+
     int nc = 0;
-
-    if (b0 <= p.eps_win) {
-        double cand = dps + d0 + b0;
-        if (cand < g0) {
-            dist_event(p, sl, it, v0, cand, ls);
-            if (v0f & SADDLE_BIT) fan_event(p, sl, it, v0, j, cand, atan2(iy, ix));
-        }
-    }
-    if (b1 >= ell - p.eps_win) {
-        double cand = dps + d1 + (ell - b1);
-        if (cand < g1) {
-            dist_event(p, sl, it, v1, cand, ls);
-            if (v1f & SADDLE_BIT) {
-                int32_t jn = 3 * (j / 3) + (j + 1) % 3;
-                fan_event(p, sl, it, v1, jn, cand, atan2(iy, ix - ell) - __ldg(&hp->adir));
-            }
-        }
-    }
-
-    const int32_t jo = __ldg(&hp->jo);
-    if (jo < 0) return 0;
-    const int32_t jno = 3 * (jo / 3) + (jo + 1) % 3;
-    const int32_t jpo = 3 * (jo / 3) + (jo + 2) % 3;
-    const double dx = __ldg(&hp->dx), dy = __ldg(&hp->dy);
-    const double lan = __ldg(&hp->lan), lpv = __ldg(&hp->lpv);
-    const uint32_t vdf = __ldg(&hp->vd);
-    const int32_t vd = (int32_t)(vdf & VMASK);
-    const double gdd = ldcg(p.dist_cur + vd);
-
-    const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
-    const double vdx = dx - ix, vdy = dy - iy;
-    const double nvd = hyp(vdx, vdy);
-    const double ca = uax * vdy - uay * vdx;
-    const double cb = ubx * vdy - uby * vdx;
-    const double tola = EPS_NUM * hyp(uax, uay) * nvd;
-    const double tolb = EPS_NUM * hyp(ubx, uby) * nvd;
+    Win tmp;
+    // children land in registers: the first in out0, the second in out1
+    auto put = [&](const Win &c) {
+        if (nc == 0) out0 = c;
+        else out1 = c;
+        ++nc;
+    };
+    bool evd = false, claim = false;
+    double candd = 0.0, comp = 0.0, entry_x = 0.0;
     double sa, sb;
+    if (jo >= 0) {
+        // unfold the far triangle: apex D below the edge (geom.py:387-516)
+        const int32_t jno = 3 * (jo / 3) + (jo + 1) % 3;
+        const int32_t jpo = 3 * (jo / 3) + (jo + 2) % 3;
+        const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
+        const double vdx = dx - ix, vdy = dy - iy;
+        const double nvd = hyp(vdx, vdy);
+        const double ca = uax * vdy - uay * vdx;
+        const double cb = ubx * vdy - uby * vdx;
+        const double tola = EPS_NUM * hyp(uax, uay) * nvd;
+        const double tolb = EPS_NUM * hyp(ubx, uby) * nvd;
+        if (ca > tola && cb < -tolb) {
+            // the ray to the apex passes strictly inside (A, B): w occupies vd
+            comp = dps + nvd;
+            const double denom = iy - dy;
+            entry_x = denom > 1e-300 ? ix + (dx - ix) * (iy / denom) : ix;
+            bool want_l = true, want_r = true;
+            if (comp < sp.x) {
+                claim = true;
+            } else {
+                // one-angle-one-split: keep only the child on our side
+                ls.add(ST_PRUNE_SPLIT);
+                ls.add(ST_CREATED);
+                if (entry_x < sp.y) want_r = false;
+                else want_l = false;
+            }
+            if (want_l) {
+                ls.add(ST_CREATED);
+                if (ray_seg(ix, iy, b0, 0.0, 0.0, 0.0, dx, dy, sa)) {
+                    int f = make_child(jno, lan, 0.0, 0.0, dx, dy, sa, 1.0, ix, iy, dps, g0, gdd, g1,
+                                       ell, 0.0, true, p.eps_win, tmp);
+                    if (f == CH_STORED) put(tmp);
+                    else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
+                } else {
+                    ls.add(ST_PRUNE_DEGEN);
+                }
+            }
+            if (want_r) {
+                ls.add(ST_CREATED);
+                if (ray_seg(ix, iy, b1, 0.0, dx, dy, ell, 0.0, sb)) {
+                    int f = make_child(jpo, lpv, dx, dy, ell, 0.0, 0.0, sb, ix, iy, dps, gdd, g1, g0,
+                                       0.0, 0.0, false, p.eps_win, tmp);
+                    if (f == CH_STORED) put(tmp);
+                    else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
+                } else {
+                    ls.add(ST_PRUNE_DEGEN);
+                }
+            }
+            candd = dps + nvd;
+            evd = candd < gdd;
+        } else {
+            ls.add(ST_CREATED);
+            const bool left = cb >= -tolb;  // both rays exit through edge v0-D
+            bool ok;
+            if (left) {
+                ok = ray_seg(ix, iy, b0, 0.0, 0.0, 0.0, dx, dy, sa) &&
+                     ray_seg(ix, iy, b1, 0.0, 0.0, 0.0, dx, dy, sb);
+            } else {
+                ok = ray_seg(ix, iy, b0, 0.0, dx, dy, ell, 0.0, sa) &&
+                     ray_seg(ix, iy, b1, 0.0, dx, dy, ell, 0.0, sb);
+            }
+            if (!ok) {
+                ls.add(ST_PRUNE_DEGEN);
+            } else {
+                int f = left ? make_child(jno, lan, 0.0, 0.0, dx, dy, sa, sb, ix, iy, dps, g0, gdd, g1,
+                                          ell, 0.0, true, p.eps_win, tmp)
+                             : make_child(jpo, lpv, dx, dy, ell, 0.0, sa, sb, ix, iy, dps, gdd, g1, g0,
+                                          0.0, 0.0, false, p.eps_win, tmp);
+                if (f == CH_STORED) put(tmp);
+                else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
+            }
+        }
+    }
 
-    if (ca > tola && cb < -tolb) {
-        // the ray to the apex passes strictly inside (A, B): w occupies vd
-        double comp = dps + nvd;
-        double denom = iy - dy;
-        double entry_x = denom > 1e-300 ? ix + (dx - ix) * (iy / denom) : ix;
-        bool want_l = true, want_r = true;
-        double2 sp = __ldcg(p.split_cur + j);
-        if (comp < sp.x) {
-            angle_event(p, sl, it, j, comp, entry_x, ls);
-        } else {
-            // one-angle-one-split: keep only the child on our side
-            ls.v[ST_PRUNE_SPLIT]++;
-            ls.v[ST_CREATED]++;
-            if (entry_x < sp.y) want_r = false;
-            else want_l = false;
-        }
-        if (want_l) {
-            ls.v[ST_CREATED]++;
-            if (ray_seg(ix, iy, b0, 0.0, 0.0, 0.0, dx, dy, sa)) {
-                int f = make_child(jno, lan, 0.0, 0.0, dx, dy, sa, 1.0, ix, iy, dps, g0, gdd, g1,
-                                   ell, 0.0, true, p.eps_win, c[nc]);
-                if (f == CH_STORED) nc++;
-                else ls.v[f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN]++;
-            } else {
-                ls.v[ST_PRUNE_DEGEN]++;
-            }
-        }
-        if (want_r) {
-            ls.v[ST_CREATED]++;
-            if (ray_seg(ix, iy, b1, 0.0, dx, dy, ell, 0.0, sb)) {
-                int f = make_child(jpo, lpv, dx, dy, ell, 0.0, 0.0, sb, ix, iy, dps, gdd, g1, g0,
-                                   0.0, 0.0, false, p.eps_win, c[nc]);
-                if (f == CH_STORED) nc++;
-                else ls.v[f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN]++;
-            } else {
-                ls.v[ST_PRUNE_DEGEN]++;
-            }
-        }
-        double cand = dps + nvd;
-        if (cand < gdd) {
-            dist_event(p, sl, it, vd, cand, ls);
-            if (vdf & SADDLE_BIT)
-                fan_event(p, sl, it, vd, jpo, cand, atan2(iy - dy, ix - dx) - __ldg(&hp->gamma));
-        }
-    } else {
-        ls.v[ST_CREATED]++;
-        bool left = cb >= -tolb;  // both rays exit through edge v0-D
-        bool ok;
-        if (left) {
-            ok = ray_seg(ix, iy, b0, 0.0, 0.0, 0.0, dx, dy, sa) &&
-                 ray_seg(ix, iy, b1, 0.0, 0.0, 0.0, dx, dy, sb);
-        } else {
-            ok = ray_seg(ix, iy, b0, 0.0, dx, dy, ell, 0.0, sa) &&
-                 ray_seg(ix, iy, b1, 0.0, dx, dy, ell, 0.0, sb);
-        }
-        if (!ok) {
-            ls.v[ST_PRUNE_DEGEN]++;
-        } else {
-            int f = left ? make_child(jno, lan, 0.0, 0.0, dx, dy, sa, sb, ix, iy, dps, g0, gdd, g1,
-                                      ell, 0.0, true, p.eps_win, c[nc])
-                         : make_child(jpo, lpv, dx, dy, ell, 0.0, sa, sb, ix, iy, dps, gdd, g1, g0,
-                                      0.0, 0.0, false, p.eps_win, c[nc]);
-            if (f == CH_STORED) nc++;
-            else ls.v[f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN]++;
-        }
+    // ---- events, issued together (order independent: min / CAS-min) ----
+    if (ev0) dist_event(p, sg, v0, cand0, ls);
+    if (ev1) dist_event(p, sg, v1, cand1, ls);
+    if (evd) dist_event(p, sg, vd, candd, ls);
+    if (claim) angle_event(p, sg, j, comp, entry_x, sp_raw, ls);
+    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, sg, it, v0, j, cand0, atan2(iy, ix));
+    if (ev1 && (v1f & SADDLE_BIT)) {
+        const int32_t jn = 3 * (j / 3) + (j + 1) % 3;
+        fan_event(p, sg, it, v1, jn, cand1, atan2(iy, ix - ell) - __ldg(&hp->adir));
+    }
+    if (evd && (vdf & SADDLE_BIT)) {
+        const int32_t jpo = 3 * (jo / 3) + (jo + 2) % 3;
+        fan_event(p, sg, it, vd, jpo, candd, atan2(iy - dy, ix - dx) - __ldg(&hp->gamma));
     }
     return nc;
 }
@@ -567,104 +732,189 @@ __device__ Thresh pick_threshold(const unsigned int *hist, double base, double w
 // ---------------------------------------------------------------------------
 // the persistent kernel
 
-__global__ void __launch_bounds__(256) pch_persistent(Params p) {
+
+__device__ __forceinline__ void trace_max(const Params &p, int it, int slot) {
+    if (p.trace && it < p.trace_cap) atomicMax(p.trace + (size_t)it * TR_N + slot, globaltimer());
+}
+
+// CTA-level allocation of `n` (<= 3) pool slots per thread for one trip:
+// one global atomicAdd per CTA; returns the thread's first slot index
+// relative to the counter (uniform: contains __syncthreads)
+__device__ __forceinline__ unsigned long long cta_alloc(unsigned long long *counter, unsigned int n) {
+    __shared__ unsigned long long s_base;
+    unsigned int total;
+    unsigned int excl = block_excl_scan(n, total);
+    if (threadIdx.x == 0) s_base = total ? atomicAdd(counter, (unsigned long long)total) : 0ull;
+    __syncthreads();
+    unsigned long long r = s_base + excl;
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ void flush_hist(unsigned int *s_hist, unsigned int *g_hist) {
+    __syncthreads();
+    for (int b = threadIdx.x; b <= NBINS; b += TPB) {
+        unsigned int x = s_hist[b];
+        if (x) {
+            atomicAdd(g_hist + b, x);
+            s_hist[b] = 0u;
+        }
+    }
+    __syncthreads();
+}
+
+#ifndef PCH_MIN_BLOCKS
+#define PCH_MIN_BLOCKS 2  // resident CTAs per SM the register budget targets
+#endif
+
+__global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) {
     Ctrl *ctrl = p.ctrl;
     unsigned int gen = 0;
-    LocalStats ls;
-    ls.zero();
+    __shared__ unsigned long long s_st[N_ST];
+    __shared__ Stage sg;
+    __shared__ unsigned int s_hist[NBINS + 1];
+    stats_init(s_st);
+    for (int b = threadIdx.x; b <= NBINS; b += TPB) s_hist[b] = 0u;
+    if (threadIdx.x == 0) sg.ntv = sg.nte = sg.nfe = 0u;
+    __syncthreads();
+    LocalStats ls{s_st};
+    int maxchild = 0;
     WinSoA X = p.X, Y = p.Y;
     double base = 0.0, w = p.w0;
-    const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const unsigned long long gthreads = (unsigned long long)gridDim.x * blockDim.x;
+    const unsigned long long gtid = (unsigned long long)blockIdx.x * TPB + threadIdx.x;
+    const unsigned long long gthreads = (unsigned long long)gridDim.x * TPB;
+    const unsigned long long nwarps = gthreads >> 5;
+    // warp-interleaved thread index: consecutive warps of work land on
+    // different CTAs (SMs), lanes of a warp stay contiguous (coalesced),
+    // so a batch much smaller than the grid still spreads over every SM
+    const unsigned long long wtid =
+        ((unsigned long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x) * 32ull + (threadIdx.x & 31);
+    const unsigned long long gwid = wtid >> 5;
+    const int lane = threadIdx.x & 31;
     const unsigned long long t_start = globaltimer();
     int it = 0;
     for (;;) {
         Slot &cur = ctrl->slot[it % 3];
         Slot &prev = ctrl->slot[(it + 2) % 3];
+        Slot &nxt = ctrl->slot[(it + 1) % 3];
         const unsigned long long nS = *(volatile unsigned long long *)&cur.nS;
         const unsigned long long nP = *(volatile unsigned long long *)&cur.nP;
+        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long *tr = p.trace + (size_t)it * TR_N;
+            tr[TR_T0] = globaltimer();
+            tr[TR_NS] = nS;
+            tr[TR_NP] = nP;
+        }
 
         // ================= phase A: propagate =================
         if (blockIdx.x == 0) {
-            Slot &nxt = ctrl->slot[(it + 1) % 3];
             if (threadIdx.x < sizeof(Slot) / 8)
                 reinterpret_cast<unsigned long long *>(&nxt)[threadIdx.x] = 0ull;
-            for (int b = threadIdx.x; b <= NBINS; b += blockDim.x) p.hist[(it + 1) & 1][b] = 0u;
-            if (threadIdx.x == 0) {
-                unsigned long long tot = nS + nP;
-                if (tot > ls.v[ST_PEAK]) ls.v[ST_PEAK] = tot;
-            }
+            for (int b = threadIdx.x; b <= NBINS; b += TPB) p.hist[(it + 1) & 1][b] = 0u;
+            if (threadIdx.x == 0) ls.max(ST_PEAK, nS + nP);
         }
         unsigned int *hcur = p.hist[it & 1];
-        auto emit_child_to_pool = [&](const Win &c) {
-            unsigned long long slot = nP + warp_alloc(&cur.nC, true);
+        // write one window into pool slot nP + rel (children C_i follow P_i)
+        auto put_pool = [&](const Win &c, unsigned long long rel) {
+            unsigned long long slot = nP + rel;
             if ((long long)slot < p.cap) {
                 store_win(X, slot, c);
-                atomicAdd(hcur + key_bin(c.key, base, w), 1u);
+                atomicAdd(s_hist + key_bin(c.key, base, w), 1u);
             } else {
                 atomicExch(&ctrl->error, ERR_OVERFLOW);
             }
-            ls.v[ST_STORED]++;
+            ls.add(ST_STORED);
         };
-        // deferred saddle fans of iteration it-1: emitted by every event
-        // whose candidate equals the committed distance and the per-vertex
-        // pick (smallest candidate, then anchor / direction)
-        if (it > 0) {
-            const unsigned long long nF = *(volatile unsigned long long *)&prev.nF;
-            const FanEv *fe = p.fanev[(it - 1) & 1];
-            const unsigned long long nFc = nF < (unsigned long long)p.fancap ? nF : p.fancap;
-            for (unsigned long long i = gtid; i < nFc; i += gthreads) {
-                FanEv e = fe[i];
-                double dv = ldcg(p.dist_cur + e.v);
-                if (__double_as_longlong(dv) != __double_as_longlong(e.cand)) continue;
-                ulonglong2 pk = __ldcg(p.fanpick[(it - 1) & 1] + e.v);
-                unsigned long long lo = ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(e.rel);
-                if (pk.x != (unsigned long long)__double_as_longlong(e.cand) || pk.y != lo) continue;
-                ls.v[ST_FANS]++;
-                emit_fan(p, e.v, e.cand, e.anchor, e.rel, false, p.dist_cur, emit_child_to_pool, ls);
-            }
-        }
-        // the selected batch
+        // (A1) the selected batch S_i: one thread per window, children into
+        // registers, pool slots reserved once per CTA and trip
         {
-            const unsigned long long nS_pad = (nS + 31ull) & ~31ull;
-            for (unsigned long long i = gtid; i < nS_pad; i += gthreads) {
-                Win c[2];
+            const unsigned long long trips = (nS + gthreads - 1) / gthreads;
+            for (unsigned long long t = 0; t < trips; ++t) {
+                const unsigned long long i = t * gthreads + wtid;
+                Win ca, cb;
                 int nc = 0;
                 if (i < nS) {
+                    long long c0 = p.prof ? clock64() : 0;
                     Win win = load_win(p.S, i);
-                    nc = propagate(p, cur, it, win, c, ls);
-                    if ((unsigned long long)nc > ls.v[ST_MAXCHILD]) ls.v[ST_MAXCHILD] = nc;
+                    nc = propagate(p, sg, it, win, ca, cb, ls);
+                    if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
+                    if (nc > maxchild) maxchild = nc;
                 }
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    bool has = q < nc;
-                    unsigned long long slot = nP + warp_alloc(&cur.nC, has);
-                    if (has) {
-                        if ((long long)slot < p.cap) {
-                            store_win(X, slot, c[q]);
-                            atomicAdd(hcur + key_bin(c[q].key, base, w), 1u);
-                        } else {
-                            atomicExch(&ctrl->error, ERR_OVERFLOW);
-                        }
-                        ls.v[ST_STORED]++;
-                    }
+                long long c2 = p.prof ? clock64() : 0;
+                const unsigned long long rel = trip_flush(p, sg, cur, it, (unsigned int)nc);
+                if (nc > 0) put_pool(ca, rel);
+                if (nc > 1) put_pool(cb, rel + 1);
+                if (p.prof) {
+                    ls.add(ST_CYC_POOL, clock64() - c2);
+                    ls.add(ST_N_POOL);
                 }
             }
         }
+        // (A2) saddle fans of iteration it-1, one warp per fan event with the
+        // lanes spread over the fan's wedges.  Only the event whose candidate
+        // is the committed distance and wins the per-vertex pick (smallest
+        // candidate, then anchor / direction) emits, so each improved saddle
+        // fans out once per improvement.
+        if (it > 0) {
+            const unsigned long long nF = *(volatile unsigned long long *)&prev.nF;
+            const unsigned long long nFc = nF < (unsigned long long)p.fancap ? nF : p.fancap;
+            const FanEv *fe = p.fanev[(it + 2) % 3];
+            const unsigned long long trips = (nFc + nwarps - 1) / nwarps;
+            for (unsigned long long t = 0; t < trips; ++t) {
+                const unsigned long long i = t * nwarps + gwid;
+                Win c;
+                unsigned int n = 0;
+                if (i < nFc) {
+                    long long c3 = p.prof ? clock64() : 0;
+                    FanEv e = fe[i];
+                    const double dv = __ldcg(p.dist_cur + e.v);
+                    const ulonglong2 pk = __ldcg(p.fanpick[(it + 2) % 3] + e.v);
+                    const unsigned long long lo =
+                        ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(e.rel);
+                    FanSpan f;
+                    if (__double_as_longlong(dv) == __double_as_longlong(e.cand) &&
+                        pk.x == (unsigned long long)__double_as_longlong(e.cand) && pk.y == lo &&
+                        fan_span(p, e.v, e.anchor, e.rel, false, f)) {
+                        if (lane == 0) ls.add(ST_FANS);
+                        const int items = f.m * f.reps;
+                        if (lane < items) {
+                            fan_item(p, e.cand, f, lane % f.m, lane / f.m, false,
+                                     [&](const Win &x) { c = x; n = 1; }, ls);
+                        }
+                        // wedges beyond the warp width (valence > 32): rare,
+                        // appended with a warp-aggregated global slot
+                        for (int q = lane + 32; q < items; q += 32)
+                            fan_item(p, e.cand, f, q % f.m, q / f.m, false,
+                                     [&](const Win &x) { put_pool(x, warp_alloc(&cur.nC, true)); }, ls);
+                    }
+                    if (p.prof) {
+                        ls.add(ST_CYC_FANITEM, clock64() - c3);
+                        ls.add(ST_N_FANITEM);
+                    }
+                }
+                unsigned long long rel = cta_alloc(&cur.nC, n);
+                if (n) put_pool(c, rel);
+            }
+        }
+        flush_hist(s_hist, hcur);
+        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_A_END);
         grid_barrier(ctrl, gen);
+        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0)
+            p.trace[(size_t)it * TR_N + TR_B1] = globaltimer();
 
         // ================= phase B: organise =================
         Thresh th = pick_threshold(hcur, base, w, p.K);
-        Slot &nxt = ctrl->slot[(it + 1) % 3];
         {
             // commit the shadow tables for entries touched this iteration
             const unsigned long long nTV = *(volatile unsigned long long *)&cur.nTV;
-            for (unsigned long long i = gtid; i < nTV; i += gthreads) {
+            const unsigned long long nTVc = nTV < (unsigned long long)p.tvcap ? nTV : p.tvcap;
+            for (unsigned long long i = gtid; i < nTVc; i += gthreads) {
                 int32_t v = __ldcg(p.tv_list + i);
                 p.dist_cur[v] = __longlong_as_double((long long)__ldcg(p.dist_new + v));
             }
             const unsigned long long nTE = *(volatile unsigned long long *)&cur.nTE;
-            for (unsigned long long i = gtid; i < nTE; i += gthreads) {
+            const unsigned long long nTEc = nTE < (unsigned long long)p.tecap ? nTE : p.tecap;
+            for (unsigned long long i = gtid; i < nTEc; i += gthreads) {
                 int32_t j = __ldcg(p.te_list + i);
                 ulonglong2 s = __ldcg(p.split_new + j);
                 p.split_cur[j] = make_double2(unord64(s.x), unord64(s.y));
@@ -672,39 +922,54 @@ __global__ void __launch_bounds__(256) pch_persistent(Params p) {
             // fan picks of iteration it-1 are consumed: reset them
             if (it > 0) {
                 const unsigned long long nF = *(volatile unsigned long long *)&prev.nF;
-                const FanEv *fe = p.fanev[(it - 1) & 1];
+                const FanEv *fe = p.fanev[(it + 2) % 3];
                 const unsigned long long nFc = nF < (unsigned long long)p.fancap ? nF : p.fancap;
                 for (unsigned long long i = gtid; i < nFc; i += gthreads)
-                    p.fanpick[(it - 1) & 1][fe[i].v] = make_ulonglong2(~0ull, ~0ull);
+                    p.fanpick[(it + 2) % 3][fe[i].v] = make_ulonglong2(~0ull, ~0ull);
             }
         }
         {
-            // partition P_i + C_i -> S_{i+1} (key <= t) and P_{i+1}
+            // partition P_i + C_i -> S_{i+1} (key <= t) and P_{i+1}: stream
+            // compaction with one reservation per CTA and trip per output
             const unsigned long long nC = *(volatile unsigned long long *)&cur.nC;
             unsigned long long total = nP + nC;
             if ((long long)total > p.cap) total = p.cap;
-            unsigned int *hnext = p.hist[(it + 1) & 1];
             const double nbase = th.t < INFINITY ? th.t : base;
-            const unsigned long long tot_pad = (total + 31ull) & ~31ull;
-            for (unsigned long long i = gtid; i < tot_pad; i += gthreads) {
+            const unsigned long long trips = (total + gthreads - 1) / gthreads;
+            __shared__ unsigned long long s_sb[2];
+            for (unsigned long long t = 0; t < trips; ++t) {
+                const unsigned long long i = t * gthreads + gtid;
+                long long c5 = p.prof ? clock64() : 0;
                 Win c;
-                bool valid = i < total;
+                const bool valid = i < total;
                 if (valid) c = load_win(X, i);
-                bool sel = valid && c.key <= th.t;
-                bool keep = valid && !sel;
-                unsigned long long si = warp_alloc(&nxt.nS, sel);
-                unsigned long long pi = warp_alloc(&nxt.nP, keep);
-                if (sel) store_win(p.S, si, c);
+                const bool sel = valid && c.key <= th.t;
+                const bool keep = valid && !sel;
+                unsigned int tot2;
+                const unsigned int ex = block_excl_scan((sel ? 1u : 0u) | (keep ? 0x10000u : 0u), tot2);
+                if (threadIdx.x == 0) {
+                    s_sb[0] = (tot2 & 0xffffu) ? atomicAdd(&nxt.nS, (unsigned long long)(tot2 & 0xffffu)) : 0ull;
+                    s_sb[1] = (tot2 >> 16) ? atomicAdd(&nxt.nP, (unsigned long long)(tot2 >> 16)) : 0ull;
+                }
+                __syncthreads();
+                if (sel) store_win(p.S, s_sb[0] + (ex & 0xffffu), c);
                 if (keep) {
-                    store_win(Y, pi, c);
-                    atomicAdd(hnext + key_bin(c.key, nbase, th.w_next), 1u);
+                    store_win(Y, s_sb[1] + (ex >> 16), c);
+                    atomicAdd(s_hist + key_bin(c.key, nbase, th.w_next), 1u);
+                }
+                __syncthreads();
+                if (p.prof && valid) {
+                    ls.add(ST_CYC_PART, clock64() - c5);
+                    ls.add(ST_N_PART);
                 }
             }
+            flush_hist(s_hist, p.hist[(it + 1) & 1]);
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             if (p.max_iter > 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
             if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
         }
+        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_B_END);
         grid_barrier(ctrl, gen);
 
         // ================= termination =================
@@ -712,6 +977,14 @@ __global__ void __launch_bounds__(256) pch_persistent(Params p) {
         const unsigned long long ns = *(volatile unsigned long long *)&nxt.nS;
         const unsigned long long np = *(volatile unsigned long long *)&nxt.nP;
         const unsigned long long nf = *(volatile unsigned long long *)&cur.nF;
+        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long *tr = p.trace + (size_t)it * TR_N;
+            tr[TR_B2] = globaltimer();
+            tr[TR_NC] = *(volatile unsigned long long *)&cur.nC;
+            tr[TR_NF] = nf;
+            tr[TR_NTV] = *(volatile unsigned long long *)&cur.nTV;
+            tr[TR_TSEL_BITS] = (unsigned long long)__double_as_longlong(th.t);
+        }
         ++it;
         if (err || (ns == 0 && np == 0 && nf == 0)) break;
         WinSoA T = X;
@@ -721,10 +994,240 @@ __global__ void __launch_bounds__(256) pch_persistent(Params p) {
         if (th.t < INFINITY) base = th.t;
         w = th.w_next;
     }
-    flush_stats(ctrl, ls);
+    if (maxchild) ls.max(ST_MAXCHILD, maxchild);
+    flush_stats(ctrl, s_st);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctrl->iterations = it;
         ctrl->t_final = base;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// The one-barrier solver (default).  Iteration i is a single phase
+// followed by one grid barrier:
+//
+//   * the threshold t_{i+1} of the next batch is fixed when the iteration
+//     starts, by a step controller that steers |S| toward k (paper §5.2's
+//     k, as a distance step instead of a k-th-key search: every CTA
+//     evaluates it identically from the same counters);
+//   * every work item is routed as it is produced: children of S_i (one
+//     thread per window), windows of P_i (re-examined against t_{i+1}) and
+//     the saddle fans won in iteration i-1 (one warp per fan, one lane per
+//     wedge) go to S_{i+1} when key <= t_{i+1}, else to P_{i+1}, through
+//     one reservation per CTA and trip (stream compaction);
+//   * events update the distance field / angle-split table atomically and
+//     the filters read them live (paper §5.1's delayed update collapses to
+//     zero delay: every value read is a real path length, so a racing read
+//     only weakens pruning).  Fields agree across runs to rounding; the
+//     bitwise-deterministic two-barrier kernel above is PCH_FLAG_DETERMINISTIC.
+
+__global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
+    Ctrl *ctrl = p.ctrl;
+    unsigned int gen = 0;
+    __shared__ unsigned long long s_st[N_ST];
+    __shared__ Stage sg;
+    __shared__ unsigned long long s_res[3];  // S / P / fan-list reservations of a trip
+    __shared__ unsigned long long s_pmin, s_smax;
+    stats_init(s_st);
+    if (threadIdx.x == 0) {
+        sg.ntv = sg.nte = sg.nfe = 0u;
+        s_pmin = ~0ull;
+        s_smax = 0ull;
+    }
+    __syncthreads();
+    LocalStats ls{s_st};
+    int maxchild = 0;
+    const unsigned long long gthreads = (unsigned long long)gridDim.x * TPB;
+    const unsigned long long nwarps = gthreads >> 5;
+    const unsigned long long gwid = (unsigned long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const unsigned long long t_start = globaltimer();
+    double t = 0.0;           // threshold S_i was selected with
+    double delta = p.delta0;  // controller step
+    int it = 0;
+    for (;;) {
+        Slot &cur = ctrl->slot[it % NSLOT];
+        Slot &nxt = ctrl->slot[(it + 1) % NSLOT];
+        Slot &prv = ctrl->slot[(it + NSLOT - 1) % NSLOT];
+        const unsigned long long nS = *(volatile unsigned long long *)&cur.nS;
+        const unsigned long long nP = *(volatile unsigned long long *)&cur.nP;
+        const unsigned long long pminb = *(volatile unsigned long long *)&cur.pmin;
+        const unsigned long long nFr = it > 0 ? *(volatile unsigned long long *)&prv.nF : 0ull;
+        const unsigned long long nF = nFr < (unsigned long long)p.fancap ? nFr : p.fancap;
+        // step controller: |S_i| / k steers the distance step
+        if (it > 0) {
+            double f = (double)p.K / (double)(nS > 0 ? nS : 1);
+            f = f < 0.5 ? 0.5 : (f > 1.5 ? 1.5 : f);
+            delta *= f;
+            delta = delta < p.delta_min ? p.delta_min : (delta > p.delta_max ? p.delta_max : delta);
+        }
+        // anchor the threshold to the data: never above the largest key
+        // actually selected (a select-all step must not run ahead), and up
+        // to the pool's smallest key when nothing was selected
+        const double pmin = nP ? __longlong_as_double((long long)pminb) : INFINITY;
+        const double smax = __longlong_as_double((long long)*(volatile unsigned long long *)&cur.smax);
+        if (nS > 0 && it > 0 && smax < t) t = smax;
+        if (nS == 0 && pmin > t && pmin < INFINITY) t = pmin;
+        const double tn = t + delta;  // threshold of S_{i+1}
+        const WinSoA Sc = (it & 1) ? p.S2 : p.S, Sn = (it & 1) ? p.S : p.S2;
+        const WinSoA Pc = (it & 1) ? p.Y : p.X, Pn = (it & 1) ? p.X : p.Y;
+        const FanEv *fev = p.fanev[(it + 1) & 1];  // fan candidates of iteration i-1
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            // the slot of iteration i+2 is idle now: clear it
+            Slot &clr = ctrl->slot[(it + 2) % NSLOT];
+            clr.nS = clr.nP = clr.nC = clr.nTV = clr.nTE = clr.nF = 0ull;
+            clr.pmin = ~0ull;
+            clr.smax = 0ull;
+            ls.max(ST_PEAK, nS + nP);
+        }
+        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long *tr = p.trace + (size_t)it * TR_N;
+            tr[TR_T0] = globaltimer();
+            tr[TR_NS] = nS;
+            tr[TR_NP] = nP;
+            tr[TR_NF] = nF;
+            tr[TR_TSEL_BITS] = (unsigned long long)__double_as_longlong(tn);
+        }
+        // route a window to S_{i+1} / P_{i+1} once its slot is known
+        auto put = [&](const WinSoA &W, unsigned long long at, const Win &c) {
+            if ((long long)at < p.cap) store_win(W, at, c);
+            else atomicExch(&ctrl->error, ERR_OVERFLOW);
+            ls.add(ST_STORED);
+        };
+        // rare path: a fan with more wedges than a warp has lanes
+        auto put_direct = [&](const Win &c) {
+            const bool sel = c.key <= tn;
+            unsigned long long si = warp_alloc(&nxt.nS, sel);
+            unsigned long long pi = warp_alloc(&nxt.nP, !sel);
+            if (sel) {
+                put(Sn, si, c);
+                atomicMax(&s_smax, (unsigned long long)__double_as_longlong(c.key));
+            } else {
+                put(Pn, pi, c);
+                atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(c.key));
+            }
+        };
+
+        // warp work items: S_i windows (32 per warp), fan candidates of i-1
+        // (one per warp), P_i windows (32 per warp)
+        const unsigned long long nwS = (nS + 31) >> 5, nwP = (nP + 31) >> 5;
+        const unsigned long long W = nwS + nF + nwP;
+        const unsigned long long trips = (W + nwarps - 1) / nwarps;
+        for (unsigned long long tr = 0; tr < trips; ++tr) {
+            const unsigned long long wi = tr * nwarps + gwid;
+            Win o0, o1;
+            int no = 0;
+            if (wi < nwS) {
+                const unsigned long long i = (wi << 5) + lane;
+                if (i < nS) {
+                    long long c0 = p.prof ? clock64() : 0;
+                    Win win = load_win(Sc, i);
+                    no = propagate(p, sg, it, win, o0, o1, ls);
+                    if (no > maxchild) maxchild = no;
+                    if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
+                }
+            } else if (wi < nwS + nF) {
+                long long c3 = p.prof ? clock64() : 0;
+                const FanEv e = fev[wi - nwS];
+                const unsigned long long dv = __ldcg(p.dist_new + e.v);
+                const ulonglong2 pk = __ldcg(p.fanpick[0] + e.v);
+                const unsigned long long hi = (unsigned long long)__double_as_longlong(e.cand);
+                const unsigned long long lo = ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(e.rel);
+                FanSpan f;
+                // the winner of the vertex's pick, still at the vertex's
+                // distance (a later improvement fans out on its own)
+                if (dv == hi && pk.x == hi && pk.y == lo && fan_span(p, e.v, e.anchor, e.rel, false, f)) {
+                    if (lane == 0) ls.add(ST_FANS);
+                    const int items = f.m * f.reps;
+                    if (lane < items)
+                        fan_item(p, e.cand, f, lane % f.m, lane / f.m, false,
+                                 [&](const Win &x) { o0 = x; no = 1; }, ls);
+                    for (int q = lane + 32; q < items; q += 32)
+                        fan_item(p, e.cand, f, q % f.m, q / f.m, false, put_direct, ls);
+                }
+                if (p.prof) {
+                    ls.add(ST_CYC_FANITEM, clock64() - c3);
+                    ls.add(ST_N_FANITEM);
+                }
+            } else if (wi < W) {
+                const unsigned long long i = ((wi - nwS - nF) << 5) + lane;
+                if (i < nP) {
+                    o0 = load_win(Pc, i);
+                    no = 1;
+                }
+            }
+            // route: S_{i+1} if key <= t_{i+1}, else P_{i+1}
+            long long c2 = p.prof ? clock64() : 0;
+            const bool s0 = no > 0 && o0.key <= tn, s1 = no > 1 && o1.key <= tn;
+            const bool k0 = no > 0 && !s0, k1 = no > 1 && !s1;
+            const unsigned int ns_ = (unsigned int)s0 + (unsigned int)s1;
+            const unsigned int np_ = (unsigned int)k0 + (unsigned int)k1;
+            if (k0) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o0.key));
+            if (k1) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o1.key));
+            if (s0) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o0.key));
+            if (s1) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o1.key));
+            unsigned int tot;
+            const unsigned int ex = block_excl_scan(ns_ | (np_ << 16), tot);
+            if (threadIdx.x == 0) {
+                s_res[0] = (tot & 0xffffu) ? atomicAdd(&nxt.nS, (unsigned long long)(tot & 0xffffu)) : 0ull;
+                s_res[1] = (tot >> 16) ? atomicAdd(&nxt.nP, (unsigned long long)(tot >> 16)) : 0ull;
+                s_res[2] = sg.nfe ? atomicAdd(&cur.nF, (unsigned long long)sg.nfe) : 0ull;
+            }
+            __syncthreads();
+            unsigned long long sa = s_res[0] + (ex & 0xffffu), pa = s_res[1] + (ex >> 16);
+            if (no > 0) {
+                if (s0) put(Sn, sa++, o0);
+                else put(Pn, pa++, o0);
+            }
+            if (no > 1) {
+                if (s1) put(Sn, sa, o1);
+                else put(Pn, pa, o1);
+            }
+            const unsigned int nfe = sg.nfe;
+            FanEv *fout = p.fanev[it & 1];
+            for (unsigned int k = threadIdx.x; k < nfe; k += TPB) {
+                unsigned long long at = s_res[2] + k;
+                if ((long long)at < p.fancap) fout[at] = sg.fe[k];
+                else atomicExch(&ctrl->error, ERR_OVERFLOW);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) sg.nfe = 0u;
+            __syncthreads();
+            if (p.prof && no > 0) {
+                ls.add(ST_CYC_POOL, clock64() - c2);
+                ls.add(ST_N_POOL);
+            }
+        }
+        if (threadIdx.x == 0) {
+            if (s_pmin != ~0ull) atomicMin(&nxt.pmin, s_pmin);
+            if (s_smax) atomicMax(&nxt.smax, s_smax);
+            s_pmin = ~0ull;
+            s_smax = 0ull;
+            if (p.trace) trace_max(p, it, TR_A_END);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if (p.max_iter > 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
+            if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
+        }
+        grid_barrier(ctrl, gen);
+        const int err = *(volatile int *)&ctrl->error;
+        const unsigned long long ns = *(volatile unsigned long long *)&nxt.nS;
+        const unsigned long long np = *(volatile unsigned long long *)&nxt.nP;
+        const unsigned long long nf = *(volatile unsigned long long *)&cur.nF;
+        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+            unsigned long long *trr = p.trace + (size_t)it * TR_N;
+            trr[TR_B1] = trr[TR_B_END] = trr[TR_B2] = globaltimer();
+            trr[TR_NC] = ns + np;
+        }
+        ++it;
+        if (err || (ns == 0 && np == 0 && nf == 0)) break;
+        t = tn;
+    }
+    if (maxchild) ls.max(ST_MAXCHILD, maxchild);
+    flush_stats(ctrl, s_st);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctrl->iterations = it;
+        ctrl->t_final = t;
     }
 }
 
@@ -737,16 +1240,17 @@ __global__ void k_init_state(Params p, const int64_t *src, int nsrc) {
     for (long long v = t0; v < p.nv; v += n) {
         p.dist_cur[v] = INFINITY;
         p.dist_new[v] = (unsigned long long)__double_as_longlong(INFINITY);
-        p.tv_stamp[v] = -1;
         p.fanpick[0][v] = make_ulonglong2(~0ull, ~0ull);
         p.fanpick[1][v] = make_ulonglong2(~0ull, ~0ull);
+        p.fanpick[2][v] = make_ulonglong2(~0ull, ~0ull);
     }
     for (long long j = t0; j < p.nhe; j += n) {
         p.split_cur[j] = make_double2(INFINITY, 0.0);
         p.split_new[j] = make_ulonglong2(ord64(INFINITY), ord64(0.0));
-        p.te_stamp[j] = -1;
     }
     for (long long b = t0; b < 2 * (NBINS + 1); b += n) (b <= NBINS ? p.hist[0][b] : p.hist[1][b - NBINS - 1]) = 0u;
+    if (t0 == 0)
+        for (int q = 0; q < NSLOT; ++q) p.ctrl->slot[q].pmin = ~0ull;
 }
 
 __global__ void k_set_sources(Params p, const int64_t *src, int nsrc) {
@@ -761,22 +1265,23 @@ __global__ void k_set_sources(Params p, const int64_t *src, int nsrc) {
 // source windows: a full fan around every source (engine.py:402 via
 // geom.py:524), into the first batch S_0
 __global__ void k_source_windows(Params p, const int64_t *src, int nsrc) {
-    LocalStats ls;
-    ls.zero();
+    __shared__ unsigned long long s_st[N_ST];
+    stats_init(s_st);
+    LocalStats ls{s_st};
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     Ctrl *ctrl = p.ctrl;
     auto emit = [&](const Win &c) {
         unsigned long long slot = atomicAdd(&ctrl->slot[0].nS, 1ull);
         if ((long long)slot < p.cap) store_win(p.S, slot, c);
         else atomicExch(&ctrl->error, ERR_OVERFLOW);
-        ls.v[ST_STORED]++;
+        ls.add(ST_STORED);
     };
     if (i < nsrc) {
         int32_t s = (int32_t)src[i];
         if (__ldg(p.fan_off + s + 1) > __ldg(p.fan_off + s))
-            emit_fan(p, s, 0.0, 0, 0.0, true, p.dist_cur, emit, ls);
+            emit_fan(p, s, 0.0, 0, 0.0, true, emit, ls);
     }
-    flush_stats(ctrl, ls);
+    flush_stats(ctrl, s_st);
 }
 
 // ---------------------------------------------------------------------------
@@ -824,8 +1329,17 @@ struct pch_mesh {
     double *d_out = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
-    int grid = 0;
+    int grid = 0, grid_live = 0;
+    unsigned long long *trace = nullptr;  // PCH_TRACE development timeline
+    long long trace_cap = 0;
 };
+
+// the final distance field of the last solve: the shadow field holds it in
+// both solvers (fp64 bit patterns of non-negative distances, +inf for
+// unreachable), the frozen copy only in the two-barrier one
+static const double *field_ptr(const pch_mesh *m) {
+    return reinterpret_cast<const double *>(m->prm.dist_new);
+}
 
 static void free_ws(pch_mesh *m) {
     for (void *q : m->ws) cudaFree(q);
@@ -875,16 +1389,21 @@ static int ensure_ws(pch_mesh *m, long long cap) {
     if ((rc = ws_alloc(m, &p.split_new, m->nhe))) return rc;
     if ((rc = ws_alloc(m, &p.fanpick[0], m->nv))) return rc;
     if ((rc = ws_alloc(m, &p.fanpick[1], m->nv))) return rc;
-    if ((rc = ws_alloc(m, &p.tv_stamp, m->nv))) return rc;
-    if ((rc = ws_alloc(m, &p.te_stamp, m->nhe))) return rc;
-    if ((rc = ws_alloc(m, &p.tv_list, m->nv))) return rc;
-    if ((rc = ws_alloc(m, &p.te_list, m->nhe))) return rc;
+    if ((rc = ws_alloc(m, &p.fanpick[2], m->nv))) return rc;
+    // one entry per improving event of an iteration (<= 3 per propagated
+    // window, <= 1 angle claim), duplicates allowed
+    p.tvcap = 3 * cap + m->nv;
+    p.tecap = cap + m->nhe;
+    if ((rc = ws_alloc(m, &p.tv_list, p.tvcap))) return rc;
+    if ((rc = ws_alloc(m, &p.te_list, p.tecap))) return rc;
     p.fancap = std::max<long long>(cap, 1 << 16);
     if ((rc = ws_alloc(m, &p.fanev[0], p.fancap))) return rc;
     if ((rc = ws_alloc(m, &p.fanev[1], p.fancap))) return rc;
+    if ((rc = ws_alloc(m, &p.fanev[2], p.fancap))) return rc;
     if ((rc = alloc_soa(m, p.X, cap))) return rc;
     if ((rc = alloc_soa(m, p.Y, cap))) return rc;
     if ((rc = alloc_soa(m, p.S, cap))) return rc;
+    if ((rc = alloc_soa(m, p.S2, cap))) return rc;
     if ((rc = ws_alloc(m, &p.hist[0], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.hist[1], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.ctrl, 1))) return rc;
@@ -913,6 +1432,19 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.time_limit_ns = 120ull * 1000000000ull;
         p.fan_full = cfg->fan_mode == 1;
         p.recheck = (cfg->flags & PCH_FLAG_NO_RECHECK) ? 0 : 1;
+        p.live = (cfg->flags & PCH_FLAG_DETERMINISTIC) ? 0 : 1;
+        p.delta0 = m->mean_edge;
+        p.delta_min = 1e-3 * m->mean_edge;
+        p.delta_max = 1e3 * m->mean_edge;
+        p.prof = getenv("PCH_PROFILE") ? 1 : 0;
+        const char *trace_path = getenv("PCH_TRACE");
+        if (trace_path && !m->trace) {
+            m->trace_cap = 1 << 17;
+            CK(cudaMalloc(&m->trace, sizeof(unsigned long long) * TR_N * m->trace_cap));
+        }
+        p.trace = trace_path ? m->trace : nullptr;
+        p.trace_cap = trace_path ? m->trace_cap : 0;
+        if (p.trace) CK(cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * TR_N * p.trace_cap, st));
         CK(cudaEventRecord(m->ev0, st));
         CK(cudaMemsetAsync(p.ctrl, 0, sizeof(Ctrl), st));
         k_init_state<<<4 * 148, 256, 0, st>>>(p, d_src, nsrc);
@@ -923,7 +1455,10 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         CK(cudaGetLastError());
         CK(cudaEventRecord(m->ev1, st));
         void *args[] = {&p};
-        CK(cudaLaunchCooperativeKernel((const void *)pch_persistent, dim3(m->grid), dim3(256), args, 0, st));
+        if (p.live)
+            CK(cudaLaunchCooperativeKernel((const void *)pch_live, dim3(m->grid_live), dim3(TPB), args, 0, st));
+        else
+            CK(cudaLaunchCooperativeKernel((const void *)pch_persistent, dim3(m->grid), dim3(TPB), args, 0, st));
         CK(cudaEventRecord(m->ev2, st));
         CK(cudaStreamSynchronize(st));
         Ctrl c;
@@ -933,6 +1468,36 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             cap *= 2;
             regrows++;
             continue;
+        }
+        if (p.trace) {
+            long long n = std::min<long long>(c.iterations, p.trace_cap);
+            std::vector<unsigned long long> h((size_t)n * TR_N);
+            CK(cudaMemcpy(h.data(), p.trace, sizeof(unsigned long long) * h.size(), cudaMemcpyDeviceToHost));
+            if (FILE *f = fopen(trace_path, "wb")) {
+                fwrite(h.data(), sizeof(unsigned long long), h.size(), f);
+                fclose(f);
+            }
+        }
+        if (p.prof) {
+            const unsigned long long *q = c.st;
+            fprintf(stderr, "PCH_PROFILE prop sections cycles/propagation: p1(load,unfold,he,g01,recheck) %.0f "
+                    "p2(end events) %.0f p3(apex classify) %.0f p4(split+angle ev) %.0f p5(children) %.0f\n",
+                    q[ST_CYC_P1] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
+                    q[ST_CYC_P2] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
+                    q[ST_CYC_P3] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
+                    q[ST_CYC_P4] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
+                    q[ST_CYC_P5] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1));
+            double np_ = (double)std::max<unsigned long long>(q[ST_PROPAGATED] + q[ST_RECHECK], 1);
+            fprintf(stderr,
+                    "PCH_PROFILE cycles/unit: load %.0f prop %.0f (events %.0f) pool %.0f "
+                    "fanspan %.0f/fan fanitem %.0f part %.0f | n_prop %.0f n_pool %llu n_fanitem %llu "
+                    "n_part %llu\n",
+                    q[ST_CYC_LOAD] / np_, q[ST_CYC_PROP] / np_, q[ST_CYC_EVENTS] / np_,
+                    q[ST_CYC_POOL] / (double)std::max<unsigned long long>(q[ST_N_POOL], 1),
+                    q[ST_CYC_FANSPAN] / (double)std::max<unsigned long long>(q[ST_FANS], 1),
+                    q[ST_CYC_FANITEM] / (double)std::max<unsigned long long>(q[ST_N_FANITEM], 1),
+                    q[ST_CYC_PART] / (double)std::max<unsigned long long>(q[ST_N_PART], 1), np_,
+                    q[ST_N_POOL], q[ST_N_FANITEM], q[ST_N_PART]);
         }
         if (c.error == ERR_GUARD)
             return fail(PCH_ERR_GUARD, "iteration cap " + std::to_string(cfg->max_iterations) + " exceeded");
@@ -1112,11 +1677,14 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
         (e = cudaEventCreate(&m->ev0)) != cudaSuccess || (e = cudaEventCreate(&m->ev1)) != cudaSuccess ||
         (e = cudaEventCreate(&m->ev2)) != cudaSuccess)
         return cleanup(PCH_ERR_CUDA, std::string("stream/event: ") + cudaGetErrorString(e));
-    int nsm = 0, per_sm = 0;
+    int nsm = 0, per_sm = 0, per_sm_live = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_persistent, 256, 0);
-    if (per_sm < 1) return cleanup(PCH_ERR_CUDA, "persistent kernel cannot be resident");
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_persistent, TPB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live, TPB, 0);
+    if (per_sm < 1 || per_sm_live < 1) return cleanup(PCH_ERR_CUDA, "persistent kernel cannot be resident");
+    // persistent grids: every SM, as many co-resident CTAs as fit (<= 4)
     m->grid = nsm * std::min(per_sm, 4);
+    m->grid_live = nsm * std::min(per_sm_live, 4);
     *out = m;
     return PCH_OK;
 }
@@ -1133,6 +1701,7 @@ int pch_mesh_destroy(pch_mesh *m) {
     cudaFree(m->fan_interior);
     cudaFree(m->d_src);
     cudaFree(m->d_out);
+    cudaFree(m->trace);
     if (m->ev0) cudaEventDestroy(m->ev0);
     if (m->ev1) cudaEventDestroy(m->ev1);
     if (m->ev2) cudaEventDestroy(m->ev2);
@@ -1170,7 +1739,7 @@ int pch_run(pch_mesh *m, const int64_t *sources, int64_t n_sources, const pch_co
     CK(cudaSetDevice(m->device));
     if ((rc = stage_sources(m, sources, n_sources))) return rc;
     if ((rc = solve(m, m->d_src, (int)n_sources, cfg, m->stream, stats))) return rc;
-    CK(cudaMemcpyAsync(out_dist, m->prm.dist_cur, sizeof(double) * m->nv, cudaMemcpyDeviceToHost, m->stream));
+    CK(cudaMemcpyAsync(out_dist, field_ptr(m), sizeof(double) * m->nv, cudaMemcpyDeviceToHost, m->stream));
     CK(cudaStreamSynchronize(m->stream));
     return PCH_OK;
 }
@@ -1183,7 +1752,7 @@ int pch_run_device(pch_mesh *m, const int64_t *d_sources, int64_t n_sources, con
     cudaStream_t st = stream ? (cudaStream_t)stream : m->stream;
     int rc = solve(m, d_sources, (int)n_sources, cfg, st, stats);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(d_out, m->prm.dist_cur, sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(d_out, field_ptr(m), sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, st));
     CK(cudaStreamSynchronize(st));
     return PCH_OK;
 }
@@ -1197,7 +1766,7 @@ int pch_run_rows(pch_mesh *m, const int64_t *sources, int64_t n_sources, const p
     if ((rc = stage_sources(m, sources, n_sources))) return rc;
     for (int64_t r = 0; r < n_sources; ++r) {
         if ((rc = solve(m, m->d_src + r, 1, cfg, m->stream, stats))) return rc;
-        CK(cudaMemcpyAsync(out_rows + r * (int64_t)m->nv, m->prm.dist_cur, sizeof(double) * m->nv,
+        CK(cudaMemcpyAsync(out_rows + r * (int64_t)m->nv, field_ptr(m), sizeof(double) * m->nv,
                            cudaMemcpyDeviceToHost, m->stream));
     }
     CK(cudaStreamSynchronize(m->stream));

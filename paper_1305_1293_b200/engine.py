@@ -43,6 +43,11 @@ class EngineConfig:
     any selection, §4.3).  ``recheck`` enables the pop-time endpoint
     re-check of the ICH filter; ``pool_capacity`` is the initial window
     pool size (0 = automatic; the pool doubles on overflow).
+    ``deterministic`` selects the two-barrier solver whose filters read
+    tables frozen at the start of each iteration (the paper's delayed
+    update): fields are then bitwise identical across runs.  The default
+    one-barrier solver reads the live tables and is faster; its fields
+    agree across runs to rounding (far inside the 1e-9 bar).
     """
 
     k: int = 4096
@@ -55,6 +60,7 @@ class EngineConfig:
     device: int = 0
     recheck: bool = True
     pool_capacity: int = 0
+    deterministic: bool = False
 
     def __post_init__(self):
         if self.k < 1:
@@ -76,7 +82,8 @@ class EngineConfig:
         c.epsilon_window = float(self.epsilon_window)
         c.max_iterations = int(self.max_iterations or 0)
         c.pool_capacity = int(self.pool_capacity)
-        c.flags = 0 if self.recheck else _native.FLAG_NO_RECHECK
+        c.flags = ((0 if self.recheck else _native.FLAG_NO_RECHECK)
+                   | (_native.FLAG_DETERMINISTIC if self.deterministic else 0))
         return c
 
 

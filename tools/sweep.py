@@ -1,0 +1,94 @@
+"""Parameter sweep of the GPU engine on a bench mesh (development tool).
+
+    python tools/sweep.py WORKLOAD "k=65536,chain_band=4;k=65536,live=1" [--trace]
+
+Each configuration is run 3 times (best device time reported) and checked
+against the sequential ICH oracle (test infrastructure, checker only).
+With --trace, PCH_TRACE is set and the per-iteration timeline of the last
+run is summarised (phase A / barrier / phase B shares).
+"""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+TR = ("t0", "a_end", "b1", "b_end", "b2", "ns", "np", "nc", "nf", "ntv", "tsel", "fan_end")
+
+
+def parse(spec):
+    out = {}
+    for kv in spec.split(","):
+        if not kv:
+            continue
+        k, v = kv.split("=")
+        out[k] = float(v) if "." in v else int(v)
+    for b in ("deterministic", "recheck"):
+        if b in out:
+            out[b] = bool(out[b])
+    return out
+
+
+def trace_summary(path):
+    a = np.fromfile(path, dtype=np.uint64).reshape(-1, len(TR)).astype(np.float64)
+    a = a[a[:, 0] > 0]
+    t0, ae, b1, be, b2 = (a[:, i] for i in range(5))
+    tot = (b2[-1] - t0[0]) / 1e3
+    ph_a = np.sum(ae - t0) / 1e3
+    bar1 = np.sum(b1 - ae) / 1e3
+    ph_b = np.sum(be - b1) / 1e3
+    bar2 = np.sum(b2 - be) / 1e3
+    ns = a[:, 5]
+    fan = np.sum(np.maximum(a[:, 11] - b1, 0)) / 1e3
+    print(f"   trace: iters={len(a)} total={tot:.0f}us A={ph_a:.0f} bar1={bar1:.0f} "
+          f"B={ph_b:.0f} bar2={bar2:.0f} | per-iter A={ph_a/len(a):.1f} B={ph_b/len(a):.1f} "
+          f"bar={(bar1+bar2)/len(a):.1f}us | nS mean={ns.mean():.0f} max={ns.max():.0f} "
+          f"nP mean={a[:, 6].mean():.0f} nC mean={a[:, 7].mean():.0f} nF mean={a[:, 8].mean():.0f} "
+          f"fan-phase={fan/len(a):.1f}us/iter", flush=True)
+
+
+def main():
+    from oracle import oracle as O
+    from paper_1305_1293_b200 import EngineConfig, run_pch
+    from paper_1305_1293_b200 import meshes as M
+    name = sys.argv[1]
+    specs = sys.argv[2].split(";")
+    trace = "--trace" in sys.argv
+    m = M.bench_mesh(name)
+    if name == "terrain1m":
+        src = 354 * 709 + 354
+    else:
+        src = int(np.argmin(np.linalg.norm(m.positions - m.positions.mean(0), axis=1)))
+    t = time.time()
+    ref, rs = O.run_ich(m, [src])
+    print(f"{name}: F={m.n_faces} src={src} ich={time.time() - t:.2f}s "
+          f"ich_windows={rs['total_windows_created']}", flush=True)
+    fin = np.isfinite(ref)
+    for spec in specs:
+        kw = parse(spec)
+        cfg = EngineConfig(**kw)
+        best = None
+        for rep in range(3):
+            if trace and rep == 2:
+                os.environ["PCH_TRACE"] = "/tmp/pch_trace.bin"
+            d, st = run_pch(m, [src], cfg)
+            os.environ.pop("PCH_TRACE", None)
+            if best is None or st.time_kernel_ms < best[1].time_kernel_ms:
+                best = (d, st)
+        d, st = best
+        same = np.array_equal(np.isfinite(d), fin)
+        err = float(np.max(np.abs(d[fin] - ref[fin]) / np.maximum(ref[fin], 1e-12))) if same else np.inf
+        print(f"{spec:40s} kern={st.time_kernel_ms:8.2f}ms dev={st.time_device_ms:8.2f}ms "
+              f"iters={st.iterations:6d} created={st.total_windows_created:10d} "
+              f"prop={st.windows_propagated:10d} fans={st.fans_emitted:8d} "
+              f"rechk={st.pruned_recheck:8d} regrow={st.buffer_regrows} err={err:.2e}",
+              flush=True)
+        if trace:
+            trace_summary("/tmp/pch_trace.bin")
+
+
+if __name__ == "__main__":
+    main()

@@ -268,7 +268,11 @@ def run_b200(args):
         e2e_ms += (time.perf_counter() - t) * 1e3
     if ws > 1:
         torch.distributed.barrier()
-    assert np.array_equal(host, field), "host and device entry points disagree"
+    # the default solver reads live tables: repeated solves agree to
+    # rounding, not bitwise; flags must be identical
+    fin = np.isfinite(field)
+    assert np.array_equal(np.isfinite(host), fin), "host and device entry points disagree"
+    assert np.all(np.abs(host[fin] - field[fin]) <= 1e-9 * np.maximum(np.abs(field[fin]), 1e-12))
 
     tot = torch.tensor([dev_ms, e2e_ms, kern_ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -297,7 +301,7 @@ def run_b200(args):
             "gpu_launches": 4 * (args.steps + regrows),
             "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 5),
-                         "traffic": traffic, "kernel": "pch_persistent",
+                         "traffic": traffic, "kernel": "pch_live",
                          "kernel_ms": round(k_ms, 4),
                          "kernel_share": round(kernel_share, 4),
                          "peak_source": peak_src,

@@ -147,33 +147,40 @@ __device__ __forceinline__ double unord64(unsigned long long b) {
     return __longlong_as_double((long long)b);
 }
 
-// Grid-wide barrier for a cooperative launch (all CTAs co-resident).  The
-// last arriver resets the counter and bumps the generation.  A waiter that
-// sees no release within 20 s flags ERR_TIMEOUT instead of hanging.
-__device__ __forceinline__ void grid_barrier(Ctrl *c, unsigned int &gen) {
+// Grid-wide barrier for a cooperative launch (all CTAs co-resident): one
+// monotonically increasing arrival counter, no separate release step --
+// thread 0 of each CTA adds its arrival (release) and spins (acquire) until
+// the counter reaches gen * gridDim.  `after` runs on thread 0 between the
+// spin and the closing __syncthreads (used to read the iteration's
+// counters once per CTA).  A waiter that sees no progress within 20 s
+// flags ERR_TIMEOUT instead of hanging.
+template <typename After>
+__device__ __forceinline__ void grid_barrier(Ctrl *c, unsigned int &gen, After &&after) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned int target = gen + 1;
+        gen += 1;
+        const unsigned int target = gen * gridDim.x;
         __threadfence();
-        unsigned int arrived = atomicAdd(&c->bar_count, 1u);
-        if (arrived == gridDim.x - 1) {
-            atomicExch(&c->bar_count, 0u);
-            __threadfence();
-            atomicExch(&c->bar_gen, target);
-        } else {
-            unsigned long long t0 = globaltimer();
-            while (ld_acquire_u32(&c->bar_gen) != target) {
-                __nanosleep(32);
-                if (globaltimer() - t0 > 20000000000ull) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&c->bar_count), "r"(1u) : "memory");
+        unsigned int spins = 0;
+        unsigned long long t0 = 0;
+        while ((int)(ld_acquire_u32(&c->bar_count) - target) < 0) {
+            if ((++spins & 1023u) == 0u) {
+                if (t0 == 0) t0 = globaltimer();
+                else if (globaltimer() - t0 > 20000000000ull) {
                     atomicExch(&c->error, ERR_TIMEOUT);
                     break;
                 }
             }
         }
         __threadfence();
-        gen = target;
+        after();
     }
     __syncthreads();
+}
+
+__device__ __forceinline__ void grid_barrier(Ctrl *c, unsigned int &gen) {
+    grid_barrier(c, gen, [] {});
 }
 
 // Warp-aggregated slot allocation among the currently active lanes:
@@ -764,7 +771,7 @@ __device__ __forceinline__ void flush_hist(unsigned int *s_hist, unsigned int *g
 }
 
 #ifndef PCH_MIN_BLOCKS
-#define PCH_MIN_BLOCKS 2  // resident CTAs per SM the register budget targets
+#define PCH_MIN_BLOCKS 1  // resident CTAs per SM the register budget targets
 #endif
 
 __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) {
@@ -1044,15 +1051,27 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
     const unsigned long long t_start = globaltimer();
     double t = 0.0;           // threshold S_i was selected with
     double delta = p.delta0;  // controller step
+    // the iteration's counters, read once per CTA by thread 0 (at the
+    // barrier) and broadcast through shared memory
+    __shared__ unsigned long long s_c[6];  // err, nS, nP, nF(prev), pmin, smax
+    if (threadIdx.x == 0) {
+        s_c[0] = 0ull;
+        s_c[1] = *(volatile unsigned long long *)&ctrl->slot[0].nS;
+        s_c[2] = *(volatile unsigned long long *)&ctrl->slot[0].nP;
+        s_c[3] = 0ull;
+        s_c[4] = *(volatile unsigned long long *)&ctrl->slot[0].pmin;
+        s_c[5] = *(volatile unsigned long long *)&ctrl->slot[0].smax;
+    }
+    __syncthreads();
     int it = 0;
     for (;;) {
         Slot &cur = ctrl->slot[it % NSLOT];
         Slot &nxt = ctrl->slot[(it + 1) % NSLOT];
-        Slot &prv = ctrl->slot[(it + NSLOT - 1) % NSLOT];
-        const unsigned long long nS = *(volatile unsigned long long *)&cur.nS;
-        const unsigned long long nP = *(volatile unsigned long long *)&cur.nP;
-        const unsigned long long pminb = *(volatile unsigned long long *)&cur.pmin;
-        const unsigned long long nFr = it > 0 ? *(volatile unsigned long long *)&prv.nF : 0ull;
+        const unsigned long long nS = s_c[1];
+        const unsigned long long nP = s_c[2];
+        const unsigned long long nFr = s_c[3];
+        const unsigned long long pminb = s_c[4];
+        const unsigned long long smaxb = s_c[5];
         const unsigned long long nF = nFr < (unsigned long long)p.fancap ? nFr : p.fancap;
         // step controller: |S_i| / k steers the distance step
         if (it > 0) {
@@ -1065,7 +1084,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
         // actually selected (a select-all step must not run ahead), and up
         // to the pool's smallest key when nothing was selected
         const double pmin = nP ? __longlong_as_double((long long)pminb) : INFINITY;
-        const double smax = __longlong_as_double((long long)*(volatile unsigned long long *)&cur.smax);
+        const double smax = __longlong_as_double((long long)smaxb);
         if (nS > 0 && it > 0 && smax < t) t = smax;
         if (nS == 0 && pmin > t && pmin < INFINITY) t = pmin;
         const double tn = t + delta;  // threshold of S_{i+1}
@@ -1209,11 +1228,18 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
             if (p.max_iter > 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
             if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
         }
-        grid_barrier(ctrl, gen);
-        const int err = *(volatile int *)&ctrl->error;
-        const unsigned long long ns = *(volatile unsigned long long *)&nxt.nS;
-        const unsigned long long np = *(volatile unsigned long long *)&nxt.nP;
-        const unsigned long long nf = *(volatile unsigned long long *)&cur.nF;
+        grid_barrier(ctrl, gen, [&] {
+            s_c[0] = (unsigned long long)*(volatile int *)&ctrl->error;
+            s_c[1] = *(volatile unsigned long long *)&nxt.nS;
+            s_c[2] = *(volatile unsigned long long *)&nxt.nP;
+            s_c[3] = *(volatile unsigned long long *)&cur.nF;
+            s_c[4] = *(volatile unsigned long long *)&nxt.pmin;
+            s_c[5] = *(volatile unsigned long long *)&nxt.smax;
+        });
+        const int err = (int)s_c[0];
+        const unsigned long long ns = s_c[1];
+        const unsigned long long np = s_c[2];
+        const unsigned long long nf = s_c[3];
         if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *trr = p.trace + (size_t)it * TR_N;
             trr[TR_B1] = trr[TR_B_END] = trr[TR_B2] = globaltimer();

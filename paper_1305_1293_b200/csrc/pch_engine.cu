@@ -84,7 +84,7 @@ struct Ctrl {
 
 struct Params {
     // mesh (immutable)
-    const HeRec *he;
+    const FaceRec *face;       // [F]
     const FanRec *fan;
     const int32_t *fan_off;    // [nv + 1]
     const int32_t *fanpos;     // [nhe] position of h in origin(h)'s fan
@@ -124,7 +124,7 @@ struct Params {
 
 // per-iteration trace record (PCH_TRACE=path): globaltimer stamps and sizes
 enum { TR_T0, TR_A_END, TR_B1, TR_B_END, TR_B2, TR_NS, TR_NP, TR_NC, TR_NF, TR_NTV, TR_TSEL_BITS,
-       TR_FAN_END, TR_N };
+       TR_FAN_END, TR_START_MAX, TR_WORK_END, TR_SCAN_END, TR_N };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -227,7 +227,7 @@ __device__ __forceinline__ int key_bin(double key, double base, double w) {
 }
 
 __device__ __forceinline__ void store_win(const WinSoA &W, unsigned long long i, const Win &c) {
-    W.he[i] = c.he;
+    W.hj[i] = make_int2(c.he, c.jo);
     W.b0[i] = c.b0;
     W.b1[i] = c.b1;
     W.d0[i] = c.d0;
@@ -238,7 +238,9 @@ __device__ __forceinline__ void store_win(const WinSoA &W, unsigned long long i,
 
 __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
     Win c;
-    c.he = __ldcg(W.he + i);
+    const int2 hj = __ldcg(W.hj + i);
+    c.he = hj.x;
+    c.jo = hj.y;
     c.b0 = __ldcg(W.b0 + i);
     c.b1 = __ldcg(W.b1 + i);
     c.d0 = __ldcg(W.d0 + i);
@@ -248,13 +250,50 @@ __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
     return c;
 }
 
-// Run counters live in shared memory (one set per CTA, flushed to Ctrl at
-// kernel exit): per-thread register or local-memory counters would cost
-// registers or an L2 round trip per increment on the propagation path.
+// Run counters.  The hot ones (ST_PROPAGATED .. ST_FANS) are packed as
+// 8-bit fields into two per-thread registers and folded into the CTA's
+// shared counters once per trip (warp sum, one shared atomic per nonzero
+// field from lane 0): a shared-memory atomic per increment serialises the
+// propagation path (measured ~25% of the solve).  Per trip a thread adds
+// at most 4 to any field, so a warp's field sum stays below 256.  The
+// others (profiling clocks, maxima) and `direct` objects go straight to
+// shared memory.
 struct LocalStats {
     unsigned long long *s;
-    __device__ __forceinline__ void add(int i, unsigned long long x = 1ull) { atomicAdd(s + i, x); }
+    bool direct;
+    unsigned long long a = 0ull, b = 0ull;
+    __device__ __forceinline__ void add(int i, unsigned long long x = 1ull) {
+        if (!direct && i <= ST_STORED) {
+            a += x << (8 * i);
+        } else if (!direct && i <= ST_FANS) {
+            b += x << (8 * (i - ST_EV_CREATED));
+        } else {
+            atomicAdd(s + i, x);
+        }
+    }
     __device__ __forceinline__ void max(int i, unsigned long long x) { atomicMax(s + i, x); }
+    // fold the packed fields into shared memory (whole warp, converged)
+    __device__ __forceinline__ void fold() {
+        unsigned long long x = a, y = b;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            x += __shfl_xor_sync(0xffffffffu, x, o);
+            y += __shfl_xor_sync(0xffffffffu, y, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int k = 0; k <= ST_STORED; ++k) {
+                unsigned long long f = (x >> (8 * k)) & 0xffull;
+                if (f) atomicAdd(s + k, f);
+            }
+#pragma unroll
+            for (int k = ST_EV_CREATED; k <= ST_FANS; ++k) {
+                unsigned long long f = (y >> (8 * (k - ST_EV_CREATED))) & 0xffull;
+                if (f) atomicAdd(s + k, f);
+            }
+        }
+        a = b = 0ull;
+    }
 };
 
 __device__ __forceinline__ void stats_init(unsigned long long *s) {
@@ -283,8 +322,13 @@ __device__ __forceinline__ void flush_stats(Ctrl *c, unsigned long long *s) {
 // memory and flushed by the CTA once per trip with one global atomic per
 // list: no hot global counter sits on the propagation path.
 
-constexpr int TPB = 256;          // threads per CTA of every solver kernel
+#ifndef PCH_TPB
+#define PCH_TPB 256
+#endif
+constexpr int TPB = PCH_TPB;      // threads per CTA of every solver kernel
 constexpr int NWARP = TPB / 32;
+constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
+constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
 struct Stage {
     unsigned int ntv, nte, nfe, pad;
@@ -488,7 +532,7 @@ __device__ __forceinline__ void fan_item(const Params &p, double cand, const Fan
         gq = gdist(p, qid);
     }
     Win c;
-    int fate = make_child(__ldg(&fr.che), __ldg(&fr.lc), px, py, qx, qy, s0, s1, 0.0, 0.0, cand,
+    int fate = make_child(__ldg(&fr.che), __ldg(&fr.cho), __ldg(&fr.lc), px, py, qx, qy, s0, s1, 0.0, 0.0, cand,
                           gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, c);
     if (fate == CH_STORED) {
         emit(c);
@@ -521,20 +565,60 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
     // (window -> half-edge record -> distances / split entry: three load
     // levels) and all event atomics are issued together at the end, fire
     // and forget where the result is not needed.
-    const int32_t j = w.he;
+    // PCH_PROFILE checkpoints: cycles until a value is available (the
+    // empty asm consumes it, so the clock read cannot move above it)
+    long long pc = 0;
+#define PCH_CKPT(ID, X)                                   \
+    if (p.prof) {                                         \
+        asm volatile("" ::"d"((double)(X)));              \
+        long long pn = clock64();                         \
+        if (ID >= 0) ls.add(ID, pn - pc);                 \
+        pc = pn;                                          \
+    }
+    PCH_CKPT(-1, 0.0);
+    const int32_t j = w.he, jo = w.jo;
     const double b0 = w.b0, b1 = w.b1, d0 = w.d0, d1 = w.d1, dps = w.d;
-    const HeRec *hp = p.he + j;
-    const double ell = __ldg(&hp->ell);
-    const uint32_t v0f = __ldg(&hp->v0), v1f = __ldg(&hp->v1), vdf = __ldg(&hp->vd);
-    const int32_t jo = __ldg(&hp->jo);
-    const double dx = __ldg(&hp->dx), dy = __ldg(&hp->dy);
-    const double lan = __ldg(&hp->lan), lpv = __ldg(&hp->lpv);
-    const int32_t v0 = (int32_t)(v0f & VMASK), v1 = (int32_t)(v1f & VMASK);
-    const int32_t vd = (int32_t)(vdf & VMASK);
-    const double g0 = gdist(p, v0), g1 = gdist(p, v1);
-    const double gdd = jo >= 0 ? gdist(p, vd) : INFINITY;
+    PCH_CKPT(ST_CYC_P1, b0 + b1 + d0 + d1 + dps + (double)jo);
+    // level 1: the far face (or, on a boundary, the window's own face)
+    // and the angle-split entry of j
+    const int32_t fr = jo >= 0 ? jo : j;
+    const int a = fr % 3;
+    const FaceRec *fp = p.face + fr / 3;
+    const int a1 = a == 2 ? 0 : a + 1, a2 = a == 0 ? 2 : a - 1;
+    double ell, lan = 0.0, lpv = 0.0;
+    uint32_t v0f, v1f, vdf = 0u;
+    int32_t cho_l = -1, cho_r = -1;
+    if (jo >= 0) {
+        // edge jo runs v1 -> v0; its successor starts at v0 (geom.py:390)
+        ell = __ldg(&fp->len[a]);
+        lan = __ldg(&fp->len[a1]);
+        lpv = __ldg(&fp->len[a2]);
+        v1f = __ldg(&fp->vid[a]);
+        v0f = __ldg(&fp->vid[a1]);
+        vdf = __ldg(&fp->vid[a2]);
+        cho_l = __ldg(&fp->opp[a1]);
+        cho_r = __ldg(&fp->opp[a2]);
+    } else {
+        ell = __ldg(&fp->len[a]);
+        v0f = __ldg(&fp->vid[a]);
+        v1f = __ldg(&fp->vid[a1]);
+    }
     ulonglong2 sp_raw = make_ulonglong2(0ull, 0ull);
     const double2 sp = jo >= 0 ? gsplit(p, j, sp_raw) : make_double2(INFINITY, 0.0);
+    // level 2: distances at the three vertices
+    const int32_t v0 = (int32_t)(v0f & VMASK), v1 = (int32_t)(v1f & VMASK);
+    const int32_t vd = (int32_t)(vdf & VMASK);
+    PCH_CKPT(ST_CYC_P2, ell + lan + lpv + (double)(v0f ^ v1f ^ vdf) + (double)(cho_l ^ cho_r) + sp.x);
+    const double g0 = gdist(p, v0), g1 = gdist(p, v1);
+    const double gdd = jo >= 0 ? gdist(p, vd) : INFINITY;
+    PCH_CKPT(ST_CYC_P3, g0 + g1 + gdd);
+    // the unfolded apex D of the far face (geom.py:394-396)
+    double dx = 0.0, dy = 0.0;
+    if (jo >= 0) {
+        dx = 0.5 * (ell * ell + lan * lan - lpv * lpv) / ell;
+        const double dy2 = lan * lan - dx * dx;
+        dy = dy2 > 0.0 ? -sqrt(dy2) : 0.0;
+    }
 
     double ix, iy;
     if (!unfold(b0, b1, d0, d1, ix, iy)) {
@@ -553,6 +637,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
         }
     }
     ls.add(ST_PROPAGATED);
+    PCH_CKPT(ST_CYC_P4, ix + iy);
 
     // interval endpoints sitting on v0 / v1 (geom.py:345-385)
     const double cand0 = dps + d0 + b0;
@@ -573,8 +658,8 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
     double sa, sb;
     if (jo >= 0) {
         // unfold the far triangle: apex D below the edge (geom.py:387-516)
-        const int32_t jno = 3 * (jo / 3) + (jo + 1) % 3;
-        const int32_t jpo = 3 * (jo / 3) + (jo + 2) % 3;
+        const int32_t jno = 3 * (jo / 3) + a1;
+        const int32_t jpo = 3 * (jo / 3) + a2;
         const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
         const double vdx = dx - ix, vdy = dy - iy;
         const double nvd = hyp(vdx, vdy);
@@ -600,7 +685,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
             if (want_l) {
                 ls.add(ST_CREATED);
                 if (ray_seg(ix, iy, b0, 0.0, 0.0, 0.0, dx, dy, sa)) {
-                    int f = make_child(jno, lan, 0.0, 0.0, dx, dy, sa, 1.0, ix, iy, dps, g0, gdd, g1,
+                    int f = make_child(jno, cho_l, lan, 0.0, 0.0, dx, dy, sa, 1.0, ix, iy, dps, g0, gdd, g1,
                                        ell, 0.0, true, p.eps_win, tmp);
                     if (f == CH_STORED) put(tmp);
                     else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
@@ -611,7 +696,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
             if (want_r) {
                 ls.add(ST_CREATED);
                 if (ray_seg(ix, iy, b1, 0.0, dx, dy, ell, 0.0, sb)) {
-                    int f = make_child(jpo, lpv, dx, dy, ell, 0.0, 0.0, sb, ix, iy, dps, gdd, g1, g0,
+                    int f = make_child(jpo, cho_r, lpv, dx, dy, ell, 0.0, 0.0, sb, ix, iy, dps, gdd, g1, g0,
                                        0.0, 0.0, false, p.eps_win, tmp);
                     if (f == CH_STORED) put(tmp);
                     else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
@@ -635,9 +720,9 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
             if (!ok) {
                 ls.add(ST_PRUNE_DEGEN);
             } else {
-                int f = left ? make_child(jno, lan, 0.0, 0.0, dx, dy, sa, sb, ix, iy, dps, g0, gdd, g1,
+                int f = left ? make_child(jno, cho_l, lan, 0.0, 0.0, dx, dy, sa, sb, ix, iy, dps, g0, gdd, g1,
                                           ell, 0.0, true, p.eps_win, tmp)
-                             : make_child(jpo, lpv, dx, dy, ell, 0.0, sa, sb, ix, iy, dps, gdd, g1, g0,
+                             : make_child(jpo, cho_r, lpv, dx, dy, ell, 0.0, sa, sb, ix, iy, dps, gdd, g1, g0,
                                           0.0, 0.0, false, p.eps_win, tmp);
                 if (f == CH_STORED) put(tmp);
                 else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
@@ -645,6 +730,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
         }
     }
 
+    PCH_CKPT(ST_CYC_P5, (nc > 0 ? out0.key : 0.0) + (nc > 1 ? out1.key : 0.0));
     // ---- events, issued together (order independent: min / CAS-min) ----
     if (ev0) dist_event(p, sg, v0, cand0, ls);
     if (ev1) dist_event(p, sg, v1, cand1, ls);
@@ -653,12 +739,22 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
     if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, sg, it, v0, j, cand0, atan2(iy, ix));
     if (ev1 && (v1f & SADDLE_BIT)) {
         const int32_t jn = 3 * (j / 3) + (j + 1) % 3;
-        fan_event(p, sg, it, v1, jn, cand1, atan2(iy, ix - ell) - __ldg(&hp->adir));
+        // direction of the source-side apex seen from v1 (geom.py:372-377)
+        const FaceRec *fj = p.face + j / 3;
+        const int b = j % 3;
+        const double lns = __ldg(&fj->len[b == 2 ? 0 : b + 1]);
+        const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
+        const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
+        const double ay2 = lps * lps - axs * axs;
+        const double adir = atan2(ay2 > 0.0 ? sqrt(ay2) : 0.0, axs - ell);
+        fan_event(p, sg, it, v1, jn, cand1, atan2(iy, ix - ell) - adir);
     }
     if (evd && (vdf & SADDLE_BIT)) {
-        const int32_t jpo = 3 * (jo / 3) + (jo + 2) % 3;
-        fan_event(p, sg, it, vd, jpo, candd, atan2(iy - dy, ix - dx) - __ldg(&hp->gamma));
+        const int32_t jpo = 3 * (jo / 3) + a2;
+        fan_event(p, sg, it, vd, jpo, candd, atan2(iy - dy, ix - dx) - atan2(-dy, ell - dx));
     }
+    PCH_CKPT(ST_CYC_EVENTS, 0.0);
+#undef PCH_CKPT
     return nc;
 }
 
@@ -674,7 +770,7 @@ __device__ Thresh pick_threshold(const unsigned int *hist, double base, double w
     __shared__ unsigned int s_part[32];
     __shared__ int s_bin;
     __shared__ unsigned long long s_total, s_over;
-    constexpr int PER = (NBINS + 255) / 256;  // blockDim is 256
+    constexpr int PER = (NBINS + TPB - 1) / TPB;
     unsigned int loc[PER];
     unsigned int sum = 0;
     int t = threadIdx.x;
@@ -784,7 +880,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
     for (int b = threadIdx.x; b <= NBINS; b += TPB) s_hist[b] = 0u;
     if (threadIdx.x == 0) sg.ntv = sg.nte = sg.nfe = 0u;
     __syncthreads();
-    LocalStats ls{s_st};
+    LocalStats ls{s_st, true};
     int maxchild = 0;
     WinSoA X = p.X, Y = p.Y;
     double base = 0.0, w = p.w0;
@@ -1034,15 +1130,17 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
     __shared__ unsigned long long s_st[N_ST];
     __shared__ Stage sg;
     __shared__ unsigned long long s_res[3];  // S / P / fan-list reservations of a trip
-    __shared__ unsigned long long s_pmin, s_smax;
+    __shared__ unsigned long long s_pmin, s_smax, s_tw;
     stats_init(s_st);
     if (threadIdx.x == 0) {
         sg.ntv = sg.nte = sg.nfe = 0u;
         s_pmin = ~0ull;
         s_smax = 0ull;
+        s_tw = 0ull;
     }
     __syncthreads();
-    LocalStats ls{s_st};
+    LocalStats ls{s_st, false};   // packed per-thread counters, folded per trip
+    LocalStats lsd{s_st, true};   // rare paths: straight to shared memory
     int maxchild = 0;
     const unsigned long long gthreads = (unsigned long long)gridDim.x * TPB;
     const unsigned long long nwarps = gthreads >> 5;
@@ -1099,6 +1197,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
             clr.smax = 0ull;
             ls.max(ST_PEAK, nS + nP);
         }
+        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_START_MAX);
         if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *tr = p.trace + (size_t)it * TR_N;
             tr[TR_T0] = globaltimer();
@@ -1113,16 +1212,19 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
             else atomicExch(&ctrl->error, ERR_OVERFLOW);
             ls.add(ST_STORED);
         };
-        // rare path: a fan with more wedges than a warp has lanes
+        // rare path: a fan with more wedges than its lane group
         auto put_direct = [&](const Win &c) {
             const bool sel = c.key <= tn;
             unsigned long long si = warp_alloc(&nxt.nS, sel);
             unsigned long long pi = warp_alloc(&nxt.nP, !sel);
+            lsd.add(ST_STORED);
             if (sel) {
-                put(Sn, si, c);
+                if ((long long)si < p.cap) store_win(Sn, si, c);
+                else atomicExch(&ctrl->error, ERR_OVERFLOW);
                 atomicMax(&s_smax, (unsigned long long)__double_as_longlong(c.key));
             } else {
-                put(Pn, pi, c);
+                if ((long long)pi < p.cap) store_win(Pn, pi, c);
+                else atomicExch(&ctrl->error, ERR_OVERFLOW);
                 atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(c.key));
             }
         };
@@ -1130,7 +1232,8 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
         // warp work items: S_i windows (32 per warp), fan candidates of i-1
         // (one per warp), P_i windows (32 per warp)
         const unsigned long long nwS = (nS + 31) >> 5, nwP = (nP + 31) >> 5;
-        const unsigned long long W = nwS + nF + nwP;
+        const unsigned long long nwF = (nF + FANS_PER_WARP - 1) / FANS_PER_WARP;
+        const unsigned long long W = nwS + nwF + nwP;
         const unsigned long long trips = (W + nwarps - 1) / nwarps;
         for (unsigned long long tr = 0; tr < trips; ++tr) {
             const unsigned long long wi = tr * nwarps + gwid;
@@ -1145,35 +1248,45 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                     if (no > maxchild) maxchild = no;
                     if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
                 }
-            } else if (wi < nwS + nF) {
+            } else if (wi < nwS + nwF) {
+                // FANS_PER_WARP candidates per warp, FAN_LANES lanes each
                 long long c3 = p.prof ? clock64() : 0;
-                const FanEv e = fev[wi - nwS];
-                const unsigned long long dv = __ldcg(p.dist_new + e.v);
-                const ulonglong2 pk = __ldcg(p.fanpick[0] + e.v);
-                const unsigned long long hi = (unsigned long long)__double_as_longlong(e.cand);
-                const unsigned long long lo = ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(e.rel);
-                FanSpan f;
-                // the winner of the vertex's pick, still at the vertex's
-                // distance (a later improvement fans out on its own)
-                if (dv == hi && pk.x == hi && pk.y == lo && fan_span(p, e.v, e.anchor, e.rel, false, f)) {
-                    if (lane == 0) ls.add(ST_FANS);
-                    const int items = f.m * f.reps;
-                    if (lane < items)
-                        fan_item(p, e.cand, f, lane % f.m, lane / f.m, false,
-                                 [&](const Win &x) { o0 = x; no = 1; }, ls);
-                    for (int q = lane + 32; q < items; q += 32)
-                        fan_item(p, e.cand, f, q % f.m, q / f.m, false, put_direct, ls);
+                const unsigned long long fi = (wi - nwS) * FANS_PER_WARP + lane / FAN_LANES;
+                const int sl = lane % FAN_LANES;
+                if (fi < nF) {
+                    const FanEv e = fev[fi];
+                    const unsigned long long dv = __ldcg(p.dist_new + e.v);
+                    const ulonglong2 pk = __ldcg(p.fanpick[0] + e.v);
+                    const unsigned long long hi = (unsigned long long)__double_as_longlong(e.cand);
+                    const unsigned long long lo = ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(e.rel);
+                    FanSpan f;
+                    // the winner of the vertex's pick, still at the vertex's
+                    // distance (a later improvement fans out on its own)
+                    if (dv == hi && pk.x == hi && pk.y == lo && fan_span(p, e.v, e.anchor, e.rel, false, f)) {
+                        if (sl == 0) ls.add(ST_FANS);
+                        const int items = f.m * f.reps;
+                        if (sl < items)
+                            fan_item(p, e.cand, f, sl % f.m, sl / f.m, false,
+                                     [&](const Win &x) { o0 = x; no = 1; }, ls);
+                        for (int q = sl + FAN_LANES; q < items; q += FAN_LANES)
+                            fan_item(p, e.cand, f, q % f.m, q / f.m, false, put_direct, lsd);
+                    }
                 }
                 if (p.prof) {
                     ls.add(ST_CYC_FANITEM, clock64() - c3);
                     ls.add(ST_N_FANITEM);
                 }
             } else if (wi < W) {
-                const unsigned long long i = ((wi - nwS - nF) << 5) + lane;
+                const unsigned long long i = ((wi - nwS - nwF) << 5) + lane;
                 if (i < nP) {
                     o0 = load_win(Pc, i);
                     no = 1;
                 }
+            }
+            if (p.trace && tr == 0) {
+                // latest end of the first trip's work over the grid
+                unsigned long long now = globaltimer();
+                atomicMax(&s_tw, now);
             }
             // route: S_{i+1} if key <= t_{i+1}, else P_{i+1}
             long long c2 = p.prof ? clock64() : 0;
@@ -1193,6 +1306,11 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 s_res[2] = sg.nfe ? atomicAdd(&cur.nF, (unsigned long long)sg.nfe) : 0ull;
             }
             __syncthreads();
+            if (p.trace && tr == 0 && threadIdx.x == 0) {
+                trace_max(p, it, TR_SCAN_END);
+                if (it < p.trace_cap) atomicMax(p.trace + (size_t)it * TR_N + TR_WORK_END, s_tw);
+                s_tw = 0ull;
+            }
             unsigned long long sa = s_res[0] + (ex & 0xffffu), pa = s_res[1] + (ex >> 16);
             if (no > 0) {
                 if (s0) put(Sn, sa++, o0);
@@ -1209,6 +1327,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 if ((long long)at < p.fancap) fout[at] = sg.fe[k];
                 else atomicExch(&ctrl->error, ERR_OVERFLOW);
             }
+            ls.fold();
             __syncthreads();
             if (threadIdx.x == 0) sg.nfe = 0u;
             __syncthreads();
@@ -1293,7 +1412,7 @@ __global__ void k_set_sources(Params p, const int64_t *src, int nsrc) {
 __global__ void k_source_windows(Params p, const int64_t *src, int nsrc) {
     __shared__ unsigned long long s_st[N_ST];
     stats_init(s_st);
-    LocalStats ls{s_st};
+    LocalStats ls{s_st, true};
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     Ctrl *ctrl = p.ctrl;
     auto emit = [&](const Win &c) {
@@ -1340,7 +1459,7 @@ struct pch_mesh {
     int device = 0;
     int32_t nv = 0, nhe = 0;
     double mean_edge = 1.0;
-    HeRec *he = nullptr;
+    FaceRec *face = nullptr;
     FanRec *fan = nullptr;
     int32_t *fan_off = nullptr, *fanpos = nullptr;
     double *fan_theta = nullptr;
@@ -1385,7 +1504,7 @@ static int ws_alloc(pch_mesh *m, T **out, size_t count) {
 
 static int alloc_soa(pch_mesh *m, WinSoA &W, long long cap) {
     int rc;
-    if ((rc = ws_alloc(m, &W.he, cap))) return rc;
+    if ((rc = ws_alloc(m, &W.hj, cap))) return rc;
     if ((rc = ws_alloc(m, &W.b0, cap))) return rc;
     if ((rc = ws_alloc(m, &W.b1, cap))) return rc;
     if ((rc = ws_alloc(m, &W.d0, cap))) return rc;
@@ -1401,7 +1520,7 @@ static int ensure_ws(pch_mesh *m, long long cap) {
     Params &p = m->prm;
     int rc;
     p = Params{};
-    p.he = m->he;
+    p.face = m->face;
     p.fan = m->fan;
     p.fan_off = m->fan_off;
     p.fanpos = m->fanpos;
@@ -1506,13 +1625,14 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         }
         if (p.prof) {
             const unsigned long long *q = c.st;
-            fprintf(stderr, "PCH_PROFILE prop sections cycles/propagation: p1(load,unfold,he,g01,recheck) %.0f "
-                    "p2(end events) %.0f p3(apex classify) %.0f p4(split+angle ev) %.0f p5(children) %.0f\n",
+            fprintf(stderr, "PCH_PROFILE prop sections cycles/propagation: window %.0f face+split %.0f "
+                    "dist %.0f unfold+recheck %.0f children %.0f events %.0f\n",
                     q[ST_CYC_P1] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
                     q[ST_CYC_P2] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
                     q[ST_CYC_P3] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
                     q[ST_CYC_P4] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
-                    q[ST_CYC_P5] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1));
+                    q[ST_CYC_P5] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
+                    q[ST_CYC_EVENTS] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1));
             double np_ = (double)std::max<unsigned long long>(q[ST_PROPAGATED] + q[ST_RECHECK], 1);
             fprintf(stderr,
                     "PCH_PROFILE cycles/unit: load %.0f prop %.0f (events %.0f) pool %.0f "
@@ -1557,7 +1677,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
 }
 
 // ---------------------------------------------------------------------------
-// mesh construction: HeRec / FanRec tables from the SurfaceMesh arrays
+// mesh construction: FaceRec / FanRec tables from the SurfaceMesh arrays
 
 static inline int64_t nxt_he(int64_t j) { return 3 * (j / 3) + (j + 1) % 3; }
 static inline int64_t prv_he(int64_t j) { return 3 * (j / 3) + (j + 2) % 3; }
@@ -1589,44 +1709,20 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
         if (opposite[j] < -1 || opposite[j] >= nhe) return fail(PCH_ERR_MESH, "opposite index out of range");
         if (!(length[j] > 0.0)) return fail(PCH_ERR_MESH, "non-positive edge length");
     }
-    std::vector<HeRec> he(nhe);
+    std::vector<FaceRec> face(n_faces);
     double lsum = 0.0;
     auto vflag = [&](int64_t v) -> uint32_t {
         return (uint32_t)v | (vertex_class[v] == 2 ? SADDLE_BIT : 0u);
     };
-    for (int64_t j = 0; j < nhe; ++j) {
-        HeRec &r = he[j];
-        int64_t jn = nxt_he(j), jp = prv_he(j);
-        double ell = length[j];
-        lsum += ell;
-        r.ell = ell;
-        r.v0 = vflag(origin[j]);
-        r.v1 = vflag(origin[jn]);
-        // direction of the source-side apex seen from v1 (geom.py:372-377)
-        double lps = length[jp], lns = length[jn];
-        double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
-        double ay2 = lps * lps - axs * axs;
-        double ays = ay2 > 0.0 ? std::sqrt(ay2) : 0.0;
-        r.adir = std::atan2(ays, axs - ell);
-        int64_t jo = opposite[j];
-        r.jo = (int32_t)jo;
-        if (jo >= 0) {
-            int64_t jno = nxt_he(jo), jpo = prv_he(jo);
-            double lan = length[jno], lpv = length[jpo];
-            double dx = 0.5 * (ell * ell + lan * lan - lpv * lpv) / ell;
-            double dy2 = lan * lan - dx * dx;
-            double dy = dy2 > 0.0 ? -std::sqrt(dy2) : 0.0;
-            r.dx = dx;
-            r.dy = dy;
-            r.lan = lan;
-            r.lpv = lpv;
-            r.vd = vflag(origin[jpo]);
-            r.gamma = std::atan2(-dy, ell - dx);
-        } else {
-            r.dx = r.dy = r.lan = r.lpv = r.gamma = 0.0;
-            r.vd = 0;
+    for (int64_t f = 0; f < n_faces; ++f) {
+        FaceRec &r = face[f];
+        for (int a = 0; a < 3; ++a) {
+            const int64_t j = 3 * f + a;
+            lsum += length[j];
+            r.len[a] = length[j];
+            r.vid[a] = vflag(origin[j]);
+            r.opp[a] = (int32_t)opposite[j];
         }
-        r.pad = 0.0;
     }
     // fan tables: for every vertex walk its outgoing half-edges
     // counterclockwise from outgoing[v] (the clockwise-most one on a
@@ -1656,6 +1752,7 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
             f.qy = lq * std::sin(f.whi);
             f.lc = length[che];
             f.che = (int32_t)che;
+            f.cho = (int32_t)opposite[che];
             f.pid = (int32_t)origin[che];
             f.qid = (int32_t)origin[hprev];
             fanpos[h] = (int32_t)(fan.size() - fan_off[v]);
@@ -1692,7 +1789,7 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
         m->mesh_bytes += bytes;
         return cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
     };
-    if ((e = up((void **)&m->he, he.data(), sizeof(HeRec) * nhe)) != cudaSuccess ||
+    if ((e = up((void **)&m->face, face.data(), sizeof(FaceRec) * n_faces)) != cudaSuccess ||
         (e = up((void **)&m->fan, fan.data(), sizeof(FanRec) * fan.size())) != cudaSuccess ||
         (e = up((void **)&m->fan_off, fan_off.data(), sizeof(int32_t) * fan_off.size())) != cudaSuccess ||
         (e = up((void **)&m->fanpos, fanpos.data(), sizeof(int32_t) * nhe)) != cudaSuccess ||
@@ -1719,7 +1816,7 @@ int pch_mesh_destroy(pch_mesh *m) {
     if (!m) return PCH_OK;
     cudaSetDevice(m->device);
     free_ws(m);
-    cudaFree(m->he);
+    cudaFree(m->face);
     cudaFree(m->fan);
     cudaFree(m->fan_off);
     cudaFree(m->fanpos);

@@ -16,7 +16,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-TR = ("t0", "a_end", "b1", "b_end", "b2", "ns", "np", "nc", "nf", "ntv", "tsel", "fan_end")
+TR = ("t0", "a_end", "b1", "b_end", "b2", "ns", "np", "nc", "nf", "ntv", "tsel", "fan_end",
+      "start_max", "work_end", "scan_end")
 
 
 def parse(spec):
@@ -48,6 +49,13 @@ def trace_summary(path):
           f"bar={(bar1+bar2)/len(a):.1f}us | nS mean={ns.mean():.0f} max={ns.max():.0f} "
           f"nP mean={a[:, 6].mean():.0f} nC mean={a[:, 7].mean():.0f} nF mean={a[:, 8].mean():.0f} "
           f"fan-phase={fan/len(a):.1f}us/iter", flush=True)
+    sm, we, se = a[:, 12], a[:, 13], a[:, 14]
+    ok = (sm > 0) & (we > 0) & (se > 0)
+    if ok.any():
+        print(f"   live split per iter: start-skew={np.mean(sm[ok] - t0[ok])/1e3:.2f}us "
+              f"work(t0->max work end)={np.mean(we[ok] - t0[ok])/1e3:.2f}us "
+              f"scan(->max scan end)={np.mean(se[ok] - we[ok])/1e3:.2f}us "
+              f"rest(->A end)={np.mean(ae[ok] - se[ok])/1e3:.2f}us", flush=True)
 
 
 def main():

@@ -560,65 +560,41 @@ __device__ void emit_fan(const Params &p, int32_t v, double cand, int32_t anchor
 
 __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, const Win &w, Win &out0,
                                          Win &out1, LocalStats &ls) {
-    // Latency layout: the per-iteration critical path is one propagation,
-    // so every memory access is issued as early as its address is known
-    // (window -> half-edge record -> distances / split entry: three load
-    // levels) and all event atomics are issued together at the end, fire
-    // and forget where the result is not needed.
-    // PCH_PROFILE checkpoints: cycles until a value is available (the
-    // empty asm consumes it, so the clock read cannot move above it)
-    long long pc = 0;
-#define PCH_CKPT(ID, X)                                   \
-    if (p.prof) {                                         \
-        asm volatile("" ::"d"((double)(X)));              \
-        long long pn = clock64();                         \
-        if (ID >= 0) ls.add(ID, pn - pc);                 \
-        pc = pn;                                          \
-    }
-    PCH_CKPT(-1, 0.0);
+    // Latency layout: the per-iteration critical path is one propagation
+    // (of the slowest lane of the slowest warp), so
+    //  * every memory access is issued as soon as its address is known
+    //    (window -> face record + split entry -> distances: three levels);
+    //  * the case analysis of Algorithm 2 selects parameters instead of
+    //    branching: both candidate children (on the far face's left and
+    //    right edge) go through one straight-line make_child each, so a
+    //    warp runs one instruction stream whatever its lanes' cases;
+    //  * all event atomics are issued together at the end, fire and forget
+    //    where the result is not needed.
     const int32_t j = w.he, jo = w.jo;
     const double b0 = w.b0, b1 = w.b1, d0 = w.d0, d1 = w.d1, dps = w.d;
-    PCH_CKPT(ST_CYC_P1, b0 + b1 + d0 + d1 + dps + (double)jo);
+    const bool far = jo >= 0;
     // level 1: the far face (or, on a boundary, the window's own face)
     // and the angle-split entry of j
-    const int32_t fr = jo >= 0 ? jo : j;
+    const int32_t fr = far ? jo : j;
     const int a = fr % 3;
     const FaceRec *fp = p.face + fr / 3;
     const int a1 = a == 2 ? 0 : a + 1, a2 = a == 0 ? 2 : a - 1;
-    double ell, lan = 0.0, lpv = 0.0;
-    uint32_t v0f, v1f, vdf = 0u;
-    int32_t cho_l = -1, cho_r = -1;
-    if (jo >= 0) {
-        // edge jo runs v1 -> v0; its successor starts at v0 (geom.py:390)
-        ell = __ldg(&fp->len[a]);
-        lan = __ldg(&fp->len[a1]);
-        lpv = __ldg(&fp->len[a2]);
-        v1f = __ldg(&fp->vid[a]);
-        v0f = __ldg(&fp->vid[a1]);
-        vdf = __ldg(&fp->vid[a2]);
-        cho_l = __ldg(&fp->opp[a1]);
-        cho_r = __ldg(&fp->opp[a2]);
-    } else {
-        ell = __ldg(&fp->len[a]);
-        v0f = __ldg(&fp->vid[a]);
-        v1f = __ldg(&fp->vid[a1]);
-    }
+    // edge jo runs v1 -> v0 and its successor starts at v0 (geom.py:390);
+    // on a boundary the record is j's own face, where j runs v0 -> v1
+    const double ell = __ldg(&fp->len[a]);
+    const double lan = __ldg(&fp->len[a1]);
+    const double lpv = __ldg(&fp->len[a2]);
+    const uint32_t va = __ldg(&fp->vid[a]), vb = __ldg(&fp->vid[a1]);
+    const uint32_t v0f = far ? vb : va, v1f = far ? va : vb;
+    const uint32_t vdf = __ldg(&fp->vid[a2]);
+    const int32_t cho_l = __ldg(&fp->opp[a1]), cho_r = __ldg(&fp->opp[a2]);
     ulonglong2 sp_raw = make_ulonglong2(0ull, 0ull);
-    const double2 sp = jo >= 0 ? gsplit(p, j, sp_raw) : make_double2(INFINITY, 0.0);
+    const double2 sp = far ? gsplit(p, j, sp_raw) : make_double2(INFINITY, 0.0);
     // level 2: distances at the three vertices
     const int32_t v0 = (int32_t)(v0f & VMASK), v1 = (int32_t)(v1f & VMASK);
     const int32_t vd = (int32_t)(vdf & VMASK);
-    PCH_CKPT(ST_CYC_P2, ell + lan + lpv + (double)(v0f ^ v1f ^ vdf) + (double)(cho_l ^ cho_r) + sp.x);
     const double g0 = gdist(p, v0), g1 = gdist(p, v1);
-    const double gdd = jo >= 0 ? gdist(p, vd) : INFINITY;
-    PCH_CKPT(ST_CYC_P3, g0 + g1 + gdd);
-    // the unfolded apex D of the far face (geom.py:394-396)
-    double dx = 0.0, dy = 0.0;
-    if (jo >= 0) {
-        dx = 0.5 * (ell * ell + lan * lan - lpv * lpv) / ell;
-        const double dy2 = lan * lan - dx * dx;
-        dy = dy2 > 0.0 ? -sqrt(dy2) : 0.0;
-    }
+    const double gdd = far ? gdist(p, vd) : INFINITY;
 
     double ix, iy;
     if (!unfold(b0, b1, d0, d1, ix, iy)) {
@@ -629,15 +605,13 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
         // endpoint inequalities of the ICH filter (paper Fig. 4b) against
         // the current field: paths through v0 (resp. v1) already reach the
         // far end of the interval more cheaply -> the window is useless
-        double tB = dps + hyp(ix - b1, iy), tA = dps + hyp(ix - b0, iy);
-        if ((g0 < INFINITY && tB > g0 + b1 + EPS_NUM) ||
-            (g1 < INFINITY && tA > g1 + (ell - b0) + EPS_NUM)) {
+        const double tB = dps + hyp(ix - b1, iy), tA = dps + hyp(ix - b0, iy);
+        if ((tB > g0 + b1 + EPS_NUM) || (tA > g1 + (ell - b0) + EPS_NUM)) {
             ls.add(ST_RECHECK);
             return 0;
         }
     }
     ls.add(ST_PROPAGATED);
-    PCH_CKPT(ST_CYC_P4, ix + iy);
 
     // interval endpoints sitting on v0 / v1 (geom.py:345-385)
     const double cand0 = dps + d0 + b0;
@@ -645,92 +619,67 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
     const double cand1 = dps + d1 + (ell - b1);
     const bool ev1 = b1 >= ell - p.eps_win && cand1 < g1;
 
+    // the far triangle: apex D below the edge (geom.py:387-516)
+    const double dx = 0.5 * (ell * ell + lan * lan - lpv * lpv) / ell;
+    const double dy2 = lan * lan - dx * dx;
+    const double dy = dy2 > 0.0 ? -sqrt(dy2) : 0.0;
+    const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
+    const double vdx = dx - ix, vdy = dy - iy;
+    const double nvd = hyp(vdx, vdy);
+    const double ca = uax * vdy - uay * vdx;
+    const double cb = ubx * vdy - uby * vdx;
+    const double tola = EPS_NUM * hyp(uax, uay) * nvd;
+    const double tolb = EPS_NUM * hyp(ubx, uby) * nvd;
+    // occ: the ray to the apex passes strictly inside (A, B) -- w occupies vd
+    const bool occ = far && ca > tola && cb < -tolb;
+    const bool left = cb >= -tolb;  // (not occ) both rays exit through edge v0-D
+    const double comp = dps + nvd;
+    const double denom = iy - dy;
+    const double entry_x = denom > 1e-300 ? ix + (dx - ix) * (iy / denom) : ix;
+    // one-angle-one-split (Fig. 4a): a stored window that already gives
+    // the apex a shorter distance leaves only the child on our side
+    const bool claim = occ && comp < sp.x;
+    const bool split_pruned = occ && !claim;
+    const bool want_l = occ ? (claim || entry_x < sp.y) : (far && left);
+    const bool want_r = occ ? (claim || !(entry_x < sp.y)) : (far && !left);
+    // the two rays: I->A against the left edge (v0, D) unless only the
+    // right edge is hit, I->B against the right edge (D, v1) unless only
+    // the left edge is hit
+    const bool eA_left = occ || left, eB_left = !occ && left;
+    double rA, rB;
+    const bool okA = ray_seg(ix, iy, b0, 0.0, eA_left ? 0.0 : dx, eA_left ? 0.0 : dy,
+                             eA_left ? dx : ell, eA_left ? dy : 0.0, rA);
+    const bool okB = ray_seg(ix, iy, b1, 0.0, eB_left ? 0.0 : dx, eB_left ? 0.0 : dy,
+                             eB_left ? dx : ell, eB_left ? dy : 0.0, rB);
+    const bool okL = okA && (occ || okB), okR = okB && (occ || okA);
+    Win cl, cr;
+    const int fl = make_child(3 * (fr / 3) + a1, cho_l, lan, 0.0, 0.0, dx, dy, rA, occ ? 1.0 : rB,
+                              ix, iy, dps, g0, gdd, g1, ell, 0.0, true, p.eps_win, cl);
+    const int frr = make_child(3 * (fr / 3) + a2, cho_r, lpv, dx, dy, ell, 0.0, occ ? 0.0 : rA, rB,
+                               ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, cr);
+    const bool ml = want_l && okL, mr = want_r && okR;  // children computed
+    const bool sl = ml && fl == CH_STORED, sr = mr && frr == CH_STORED;
+    // accounting as the reference counts it (geom.py:433-516)
+    ls.add(ST_PRUNE_SPLIT, split_pruned ? 1 : 0);
+    ls.add(ST_CREATED, (split_pruned ? 1 : 0) + (occ ? (want_l ? 1 : 0) + (want_r ? 1 : 0) : (far ? 1 : 0)));
+    const unsigned int degen = occ ? (want_l && !okL ? 1u : 0u) + (want_r && !okR ? 1u : 0u)
+                                   : (far && !(okA && okB) ? 1u : 0u);
+    ls.add(ST_PRUNE_DEGEN, degen + (ml && fl == CH_DEGEN ? 1u : 0u) + (mr && frr == CH_DEGEN ? 1u : 0u));
+    ls.add(ST_PRUNE_TINY, (ml && fl == CH_TINY ? 1u : 0u) + (mr && frr == CH_TINY ? 1u : 0u));
+    ls.add(ST_PRUNE_ICH, (ml && fl == CH_ICH ? 1u : 0u) + (mr && frr == CH_ICH ? 1u : 0u));
     int nc = 0;
-    Win tmp;
-    // children land in registers: the first in out0, the second in out1
-    auto put = [&](const Win &c) {
-        if (nc == 0) out0 = c;
-        else out1 = c;
-        ++nc;
-    };
-    bool evd = false, claim = false;
-    double candd = 0.0, comp = 0.0, entry_x = 0.0;
-    double sa, sb;
-    if (jo >= 0) {
-        // unfold the far triangle: apex D below the edge (geom.py:387-516)
-        const int32_t jno = 3 * (jo / 3) + a1;
-        const int32_t jpo = 3 * (jo / 3) + a2;
-        const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
-        const double vdx = dx - ix, vdy = dy - iy;
-        const double nvd = hyp(vdx, vdy);
-        const double ca = uax * vdy - uay * vdx;
-        const double cb = ubx * vdy - uby * vdx;
-        const double tola = EPS_NUM * hyp(uax, uay) * nvd;
-        const double tolb = EPS_NUM * hyp(ubx, uby) * nvd;
-        if (ca > tola && cb < -tolb) {
-            // the ray to the apex passes strictly inside (A, B): w occupies vd
-            comp = dps + nvd;
-            const double denom = iy - dy;
-            entry_x = denom > 1e-300 ? ix + (dx - ix) * (iy / denom) : ix;
-            bool want_l = true, want_r = true;
-            if (comp < sp.x) {
-                claim = true;
-            } else {
-                // one-angle-one-split: keep only the child on our side
-                ls.add(ST_PRUNE_SPLIT);
-                ls.add(ST_CREATED);
-                if (entry_x < sp.y) want_r = false;
-                else want_l = false;
-            }
-            if (want_l) {
-                ls.add(ST_CREATED);
-                if (ray_seg(ix, iy, b0, 0.0, 0.0, 0.0, dx, dy, sa)) {
-                    int f = make_child(jno, cho_l, lan, 0.0, 0.0, dx, dy, sa, 1.0, ix, iy, dps, g0, gdd, g1,
-                                       ell, 0.0, true, p.eps_win, tmp);
-                    if (f == CH_STORED) put(tmp);
-                    else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
-                } else {
-                    ls.add(ST_PRUNE_DEGEN);
-                }
-            }
-            if (want_r) {
-                ls.add(ST_CREATED);
-                if (ray_seg(ix, iy, b1, 0.0, dx, dy, ell, 0.0, sb)) {
-                    int f = make_child(jpo, cho_r, lpv, dx, dy, ell, 0.0, 0.0, sb, ix, iy, dps, gdd, g1, g0,
-                                       0.0, 0.0, false, p.eps_win, tmp);
-                    if (f == CH_STORED) put(tmp);
-                    else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
-                } else {
-                    ls.add(ST_PRUNE_DEGEN);
-                }
-            }
-            candd = dps + nvd;
-            evd = candd < gdd;
-        } else {
-            ls.add(ST_CREATED);
-            const bool left = cb >= -tolb;  // both rays exit through edge v0-D
-            bool ok;
-            if (left) {
-                ok = ray_seg(ix, iy, b0, 0.0, 0.0, 0.0, dx, dy, sa) &&
-                     ray_seg(ix, iy, b1, 0.0, 0.0, 0.0, dx, dy, sb);
-            } else {
-                ok = ray_seg(ix, iy, b0, 0.0, dx, dy, ell, 0.0, sa) &&
-                     ray_seg(ix, iy, b1, 0.0, dx, dy, ell, 0.0, sb);
-            }
-            if (!ok) {
-                ls.add(ST_PRUNE_DEGEN);
-            } else {
-                int f = left ? make_child(jno, cho_l, lan, 0.0, 0.0, dx, dy, sa, sb, ix, iy, dps, g0, gdd, g1,
-                                          ell, 0.0, true, p.eps_win, tmp)
-                             : make_child(jpo, cho_r, lpv, dx, dy, ell, 0.0, sa, sb, ix, iy, dps, gdd, g1, g0,
-                                          0.0, 0.0, false, p.eps_win, tmp);
-                if (f == CH_STORED) put(tmp);
-                else ls.add(f == CH_TINY ? ST_PRUNE_TINY : f == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
-            }
-        }
+    if (sl) {
+        out0 = cl;
+        nc = 1;
     }
+    if (sr) {
+        if (nc) out1 = cr;
+        else out0 = cr;
+        ++nc;
+    }
+    const double candd = comp;
+    const bool evd = occ && candd < gdd;
 
-    PCH_CKPT(ST_CYC_P5, (nc > 0 ? out0.key : 0.0) + (nc > 1 ? out1.key : 0.0));
     // ---- events, issued together (order independent: min / CAS-min) ----
     if (ev0) dist_event(p, sg, v0, cand0, ls);
     if (ev1) dist_event(p, sg, v1, cand1, ls);
@@ -749,12 +698,8 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
         const double adir = atan2(ay2 > 0.0 ? sqrt(ay2) : 0.0, axs - ell);
         fan_event(p, sg, it, v1, jn, cand1, atan2(iy, ix - ell) - adir);
     }
-    if (evd && (vdf & SADDLE_BIT)) {
-        const int32_t jpo = 3 * (jo / 3) + a2;
-        fan_event(p, sg, it, vd, jpo, candd, atan2(iy - dy, ix - dx) - atan2(-dy, ell - dx));
-    }
-    PCH_CKPT(ST_CYC_EVENTS, 0.0);
-#undef PCH_CKPT
+    if (evd && (vdf & SADDLE_BIT))
+        fan_event(p, sg, it, vd, 3 * (jo / 3) + a2, candd, atan2(iy - dy, ix - dx) - atan2(-dy, ell - dx));
     return nc;
 }
 

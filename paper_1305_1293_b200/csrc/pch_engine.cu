@@ -86,10 +86,8 @@ struct Params {
     // mesh (immutable)
     const FaceRec *face;       // [F]
     const FanRec *fan;
-    const int32_t *fan_off;    // [nv + 1]
-    const int32_t *fanpos;     // [nhe] position of h in origin(h)'s fan
-    const double *fan_theta;   // [nv]
-    const uint8_t *fan_interior;  // [nv]
+    const FanHdr *fanhdr;      // [nv] wedge range, total angle, interior flag
+    const double *anchor_wlo;  // [nhe] start angle of h's wedge in origin(h)'s fan
     int32_t nv, nhe;
     // distance field / angle-split table: frozen + shadow copies
     double *dist_cur;
@@ -124,7 +122,7 @@ struct Params {
 
 // per-iteration trace record (PCH_TRACE=path): globaltimer stamps and sizes
 enum { TR_T0, TR_A_END, TR_B1, TR_B_END, TR_B2, TR_NS, TR_NP, TR_NC, TR_NF, TR_NTV, TR_TSEL_BITS,
-       TR_FAN_END, TR_START_MAX, TR_WORK_END, TR_SCAN_END, TR_N };
+       TR_FAN_END, TR_START_MAX, TR_WORK_END, TR_SCAN_END, TR_TRIP0, TR_LOADED, TR_N };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -330,11 +328,13 @@ constexpr int NWARP = TPB / 32;
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
+constexpr int FE_CAP = 2 * TPB;
+
 struct Stage {
     unsigned int ntv, nte, nfe, pad;
     int32_t tv[3 * TPB];  // improved vertices (<= 3 per propagation)
     int32_t te[TPB];      // improved angle-split entries (<= 1)
-    FanEv fe[3 * TPB];    // saddle fan candidates (<= 3)
+    FanEv fe[FE_CAP];     // saddle fan candidates (overflow appends directly)
 };
 
 __device__ __forceinline__ void dist_event(const Params &p, Stage &sg, int32_t v, double cand,
@@ -362,19 +362,36 @@ __device__ __forceinline__ void angle_event(const Params &p, Stage &sg, int32_t 
     }
 }
 
-__device__ __forceinline__ void fan_event(const Params &p, Stage &sg, int it, int32_t v,
-                                          int32_t anchor, double cand, double rel) {
-    unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
-    unsigned long long lo = ((unsigned long long)(uint32_t)anchor << 32) | ord_hi32(rel);
-    // picks start at (~0, ~0): the first claim of an iteration succeeds
-    // in one round trip
-    cas_min_u128(p.fanpick[p.live ? 0 : it % 3] + v, hi, lo, make_ulonglong2(~0ull, ~0ull));
-    unsigned int k = atomicAdd(&sg.nfe, 1u);
-    FanEv &e = sg.fe[k];
+__device__ __forceinline__ void fan_event(const Params &p, Stage &sg, int it, unsigned long long *nf_glob,
+                                          FanEv *fe_out, ulonglong2 guess, int32_t v, int32_t anchor,
+                                          double cand, double ax, double ay, double bx, double by) {
+    FanEv e;
     e.v = v;
     e.anchor = anchor;
     e.cand = cand;
-    e.rel = rel;
+    e.ax = ax;
+    e.ay = ay;
+    e.bx = bx;
+    e.by = by;
+    // per-vertex pick (smallest candidate, then anchor / direction) by
+    // 128-bit CAS-min: ties are common (the same pseudo source reaching a
+    // saddle through several windows) and every tying event would emit the
+    // same fan (the reference dedupes those rows, engine.py:201).  The
+    // deterministic solver resets the picks every iteration; the live one
+    // never does (a new candidate is always strictly smaller) and seeds the
+    // CAS with the pick it read, so a claim is one round trip.
+    const unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
+    const unsigned long long lo = ((unsigned long long)(uint32_t)anchor << 32) | ord_hi32(fan_rel(e));
+    cas_min_u128(p.fanpick[p.live ? 0 : it % 3] + v, hi, lo, guess);
+    const unsigned int k = atomicAdd(&sg.nfe, 1u);
+    if (k < (unsigned int)FE_CAP) {
+        sg.fe[k] = e;
+    } else {
+        atomicSub(&sg.nfe, 1u);
+        const unsigned long long at = atomicAdd(nf_glob, 1ull);
+        if ((long long)at < p.fancap) fe_out[at] = e;
+        else atomicExch(&p.ctrl->error, ERR_OVERFLOW);
+    }
 }
 
 // End of one trip of the selected batch (uniform over the CTA): reserve
@@ -392,11 +409,11 @@ __device__ __forceinline__ unsigned long long trip_flush(const Params &p, Stage 
     if (threadIdx.x == 0) {
         s_b[0] = sg.ntv ? atomicAdd(&sl.nTV, (unsigned long long)sg.ntv) : 0ull;
         s_b[1] = sg.nte ? atomicAdd(&sl.nTE, (unsigned long long)sg.nte) : 0ull;
-        s_b[2] = sg.nfe ? atomicAdd(&sl.nF, (unsigned long long)sg.nfe) : 0ull;
+        s_b[2] = sg.nfe ? atomicAdd(&sl.nF, (unsigned long long)min(sg.nfe, (unsigned int)FE_CAP)) : 0ull;
         s_b[3] = total ? atomicAdd(&sl.nC, (unsigned long long)total) : 0ull;
     }
     __syncthreads();
-    const unsigned int ntv = sg.ntv, nte = sg.nte, nfe = sg.nfe;
+    const unsigned int ntv = sg.ntv, nte = sg.nte, nfe = min(sg.nfe, (unsigned int)FE_CAP);
     for (unsigned int k = threadIdx.x; k < ntv; k += TPB) {
         unsigned long long at = s_b[0] + k;
         if ((long long)at < p.tvcap) p.tv_list[at] = sg.tv[k];
@@ -462,9 +479,15 @@ struct FanSpan {
 // fan interval of v (geom.py:239-256); returns false for an empty fan
 __device__ __forceinline__ bool fan_span(const Params &p, int32_t v, int32_t anchor, double rel,
                                          bool full, FanSpan &f) {
-    f.off = __ldg(p.fan_off + v);
-    f.m = __ldg(p.fan_off + v + 1) - f.off;
-    f.theta = __ldg(p.fan_theta + v);
+    // one 16-byte header per vertex and the anchor's wedge angle: both
+    // addresses are known from the event, so the two loads overlap
+    const double2 hraw = __ldg(reinterpret_cast<const double2 *>(p.fanhdr + v));
+    const double aphi = full ? 0.0 : __ldg(p.anchor_wlo + anchor);
+    f.theta = hraw.x;
+    const long long meta = __double_as_longlong(hraw.y);
+    f.off = (int32_t)(meta & 0xffffffffll);
+    f.m = (int32_t)((meta >> 32) & 0x7fffffffll);
+    const bool interior = (meta >> 63) & 1;
     if (full) {
         f.flo = -1.0e300;
         f.fhi = 1.0e300;
@@ -473,10 +496,9 @@ __device__ __forceinline__ bool fan_span(const Params &p, int32_t v, int32_t anc
     }
     double width = f.theta - TWO_PI_D;
     if (width <= EPS_NUM) return false;
-    double aphi = __ldg(&p.fan[f.off + __ldg(p.fanpos + anchor)].wlo);
     f.flo = aphi + rel + PI_D;
     f.fhi = f.flo + width;
-    if (__ldg(p.fan_interior + v)) {
+    if (interior) {
         double k = floor(f.flo / f.theta);
         f.flo -= k * f.theta;
         f.fhi -= k * f.theta;
@@ -558,8 +580,9 @@ __device__ void emit_fan(const Params &p, int32_t v, double cand, int32_t anchor
 // Algorithm 2 (geom.py:312) for one window against the frozen tables.
 // Up to two children are returned in `c`; events go to the shadow tables.
 
-__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, const Win &w, Win &out0,
-                                         Win &out1, LocalStats &ls) {
+__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, unsigned long long *nf_glob,
+                                         FanEv *fe_out, const Win &w, Win &out0, Win &out1,
+                                         LocalStats &ls) {
     // Latency layout: the per-iteration critical path is one propagation
     // (of the slowest lane of the slowest warp), so
     //  * every memory access is issued as soon as its address is known
@@ -595,6 +618,12 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
     const int32_t vd = (int32_t)(vdf & VMASK);
     const double g0 = gdist(p, v0), g1 = gdist(p, v1);
     const double gdd = far ? gdist(p, vd) : INFINITY;
+    // saddle endpoints: the current fan pick, the guess for its CAS-min
+    const ulonglong2 *pick = p.fanpick[p.live ? 0 : it % 3];
+    const ulonglong2 none = make_ulonglong2(~0ull, ~0ull);
+    const ulonglong2 pk0 = (p.live && (v0f & SADDLE_BIT)) ? __ldcg(pick + v0) : none;
+    const ulonglong2 pk1 = (p.live && (v1f & SADDLE_BIT)) ? __ldcg(pick + v1) : none;
+    const ulonglong2 pkd = (p.live && far && (vdf & SADDLE_BIT)) ? __ldcg(pick + vd) : none;
 
     double ix, iy;
     if (!unfold(b0, b1, d0, d1, ix, iy)) {
@@ -685,21 +714,31 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, con
     if (ev1) dist_event(p, sg, v1, cand1, ls);
     if (evd) dist_event(p, sg, vd, candd, ls);
     if (claim) angle_event(p, sg, j, comp, entry_x, sp_raw, ls);
-    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, sg, it, v0, j, cand0, atan2(iy, ix));
+    // saddle fans (Fig. 3c): the reverse direction of the incoming ray
+    // relative to an anchor half-edge out of the vertex (geom.py:353-484)
+    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, sg, it, nf_glob, fe_out, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
     if (ev1 && (v1f & SADDLE_BIT)) {
-        const int32_t jn = 3 * (j / 3) + (j + 1) % 3;
-        // direction of the source-side apex seen from v1 (geom.py:372-377)
-        const FaceRec *fj = p.face + j / 3;
-        const int b = j % 3;
-        const double lns = __ldg(&fj->len[b == 2 ? 0 : b + 1]);
-        const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
-        const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
-        const double ay2 = lps * lps - axs * axs;
-        const double adir = atan2(ay2 > 0.0 ? sqrt(ay2) : 0.0, axs - ell);
-        fan_event(p, sg, it, v1, jn, cand1, atan2(iy, ix - ell) - adir);
+        if (far) {
+            // anchor jo = v1 -> v0: its wedge follows next(j)'s, so this is
+            // the reference's anchor next(j) with the corner at v1 folded
+            // into the anchor angle
+            fan_event(p, sg, it, nf_glob, fe_out, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
+        } else {
+            // boundary window: anchor next(j), the source-side apex
+            // direction from v1 (geom.py:372-377)
+            const int32_t jn = 3 * (j / 3) + (j + 1) % 3;
+            const FaceRec *fj = p.face + j / 3;
+            const int b = j % 3;
+            const double lns = __ldg(&fj->len[b == 2 ? 0 : b + 1]);
+            const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
+            const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
+            const double ay2 = lps * lps - axs * axs;
+            fan_event(p, sg, it, nf_glob, fe_out, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
+                      ay2 > 0.0 ? sqrt(ay2) : 0.0);
+        }
     }
     if (evd && (vdf & SADDLE_BIT))
-        fan_event(p, sg, it, vd, 3 * (jo / 3) + a2, candd, atan2(iy - dy, ix - dx) - atan2(-dy, ell - dx));
+        fan_event(p, sg, it, nf_glob, fe_out, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
     return nc;
 }
 
@@ -884,7 +923,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 if (i < nS) {
                     long long c0 = p.prof ? clock64() : 0;
                     Win win = load_win(p.S, i);
-                    nc = propagate(p, sg, it, win, ca, cb, ls);
+                    nc = propagate(p, sg, it, &cur.nF, p.fanev[it % 3], win, ca, cb, ls);
                     if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
                     if (nc > maxchild) maxchild = nc;
                 }
@@ -915,14 +954,15 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 if (i < nFc) {
                     long long c3 = p.prof ? clock64() : 0;
                     FanEv e = fe[i];
+                    const double rel = fan_rel(e);
                     const double dv = __ldcg(p.dist_cur + e.v);
                     const ulonglong2 pk = __ldcg(p.fanpick[(it + 2) % 3] + e.v);
                     const unsigned long long lo =
-                        ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(e.rel);
+                        ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(rel);
                     FanSpan f;
                     if (__double_as_longlong(dv) == __double_as_longlong(e.cand) &&
                         pk.x == (unsigned long long)__double_as_longlong(e.cand) && pk.y == lo &&
-                        fan_span(p, e.v, e.anchor, e.rel, false, f)) {
+                        fan_span(p, e.v, e.anchor, rel, false, f)) {
                         if (lane == 0) ls.add(ST_FANS);
                         const int items = f.m * f.reps;
                         if (lane < items) {
@@ -1075,13 +1115,13 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
     __shared__ unsigned long long s_st[N_ST];
     __shared__ Stage sg;
     __shared__ unsigned long long s_res[3];  // S / P / fan-list reservations of a trip
-    __shared__ unsigned long long s_pmin, s_smax, s_tw;
+    __shared__ unsigned long long s_pmin, s_smax, s_tw, s_tl, s_tf;
     stats_init(s_st);
     if (threadIdx.x == 0) {
         sg.ntv = sg.nte = sg.nfe = 0u;
         s_pmin = ~0ull;
         s_smax = 0ull;
-        s_tw = 0ull;
+        s_tw = s_tl = s_tf = 0ull;
     }
     __syncthreads();
     LocalStats ls{s_st, false};   // packed per-thread counters, folded per trip
@@ -1179,8 +1219,11 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
         const unsigned long long nwS = (nS + 31) >> 5, nwP = (nP + 31) >> 5;
         const unsigned long long nwF = (nF + FANS_PER_WARP - 1) / FANS_PER_WARP;
         const unsigned long long W = nwS + nwF + nwP;
-        const unsigned long long trips = (W + nwarps - 1) / nwarps;
-        for (unsigned long long tr = 0; tr < trips; ++tr) {
+        // counts stay far below 2^32: 32-bit division (a 64-bit one is a
+        // software routine on the critical path of every iteration)
+        const unsigned int trips = ((unsigned int)W + (unsigned int)nwarps - 1u) / (unsigned int)nwarps;
+        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_TRIP0);
+        for (unsigned int tr = 0; tr < trips; ++tr) {
             const unsigned long long wi = tr * nwarps + gwid;
             Win o0, o1;
             int no = 0;
@@ -1189,7 +1232,11 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 if (i < nS) {
                     long long c0 = p.prof ? clock64() : 0;
                     Win win = load_win(Sc, i);
-                    no = propagate(p, sg, it, win, o0, o1, ls);
+                    if (p.trace && tr == 0) {
+                        asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
+                        atomicMax(&s_tl, globaltimer());
+                    }
+                    no = propagate(p, sg, it, &cur.nF, p.fanev[it & 1], win, o0, o1, ls);
                     if (no > maxchild) maxchild = no;
                     if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
                 }
@@ -1202,12 +1249,16 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                     const FanEv e = fev[fi];
                     const unsigned long long dv = __ldcg(p.dist_new + e.v);
                     const ulonglong2 pk = __ldcg(p.fanpick[0] + e.v);
+                    const double rel = fan_rel(e);
                     const unsigned long long hi = (unsigned long long)__double_as_longlong(e.cand);
-                    const unsigned long long lo = ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(e.rel);
+                    const unsigned long long lo = ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(rel);
+                    // the fan's span is read speculatively, in parallel with
+                    // the winner check: the winner of the vertex's pick,
+                    // still at the vertex's distance (a later improvement
+                    // fans out on its own)
                     FanSpan f;
-                    // the winner of the vertex's pick, still at the vertex's
-                    // distance (a later improvement fans out on its own)
-                    if (dv == hi && pk.x == hi && pk.y == lo && fan_span(p, e.v, e.anchor, e.rel, false, f)) {
+                    const bool span = fan_span(p, e.v, e.anchor, rel, false, f);
+                    if (dv == hi && pk.x == hi && pk.y == lo && span) {
                         if (sl == 0) ls.add(ST_FANS);
                         const int items = f.m * f.reps;
                         if (sl < items)
@@ -1229,9 +1280,11 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 }
             }
             if (p.trace && tr == 0) {
-                // latest end of the first trip's work over the grid
+                // latest end of the first trip's work over the grid (S
+                // windows) and of the fan warps (TR_FAN_END)
                 unsigned long long now = globaltimer();
-                atomicMax(&s_tw, now);
+                if (wi < nwS) atomicMax(&s_tw, now);
+                else if (wi < nwS + nwF) atomicMax(&s_tf, now);
             }
             // route: S_{i+1} if key <= t_{i+1}, else P_{i+1}
             long long c2 = p.prof ? clock64() : 0;
@@ -1248,13 +1301,17 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
             if (threadIdx.x == 0) {
                 s_res[0] = (tot & 0xffffu) ? atomicAdd(&nxt.nS, (unsigned long long)(tot & 0xffffu)) : 0ull;
                 s_res[1] = (tot >> 16) ? atomicAdd(&nxt.nP, (unsigned long long)(tot >> 16)) : 0ull;
-                s_res[2] = sg.nfe ? atomicAdd(&cur.nF, (unsigned long long)sg.nfe) : 0ull;
+                s_res[2] = sg.nfe ? atomicAdd(&cur.nF, (unsigned long long)min(sg.nfe, (unsigned int)FE_CAP)) : 0ull;
             }
             __syncthreads();
             if (p.trace && tr == 0 && threadIdx.x == 0) {
                 trace_max(p, it, TR_SCAN_END);
-                if (it < p.trace_cap) atomicMax(p.trace + (size_t)it * TR_N + TR_WORK_END, s_tw);
-                s_tw = 0ull;
+                if (it < p.trace_cap) {
+                    atomicMax(p.trace + (size_t)it * TR_N + TR_WORK_END, s_tw);
+                    atomicMax(p.trace + (size_t)it * TR_N + TR_LOADED, s_tl);
+                    atomicMax(p.trace + (size_t)it * TR_N + TR_FAN_END, s_tf);
+                }
+                s_tw = s_tl = s_tf = 0ull;
             }
             unsigned long long sa = s_res[0] + (ex & 0xffffu), pa = s_res[1] + (ex >> 16);
             if (no > 0) {
@@ -1265,7 +1322,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 if (s1) put(Sn, sa, o1);
                 else put(Pn, pa, o1);
             }
-            const unsigned int nfe = sg.nfe;
+            const unsigned int nfe = min(sg.nfe, (unsigned int)FE_CAP);
             FanEv *fout = p.fanev[it & 1];
             for (unsigned int k = threadIdx.x; k < nfe; k += TPB) {
                 unsigned long long at = s_res[2] + k;
@@ -1368,7 +1425,7 @@ __global__ void k_source_windows(Params p, const int64_t *src, int nsrc) {
     };
     if (i < nsrc) {
         int32_t s = (int32_t)src[i];
-        if (__ldg(p.fan_off + s + 1) > __ldg(p.fan_off + s))
+        if ((__double_as_longlong(__ldg(&p.fanhdr[s].meta_bits)) >> 32) & 0x7fffffffll)
             emit_fan(p, s, 0.0, 0, 0.0, true, emit, ls);
     }
     flush_stats(ctrl, s_st);
@@ -1406,9 +1463,8 @@ struct pch_mesh {
     double mean_edge = 1.0;
     FaceRec *face = nullptr;
     FanRec *fan = nullptr;
-    int32_t *fan_off = nullptr, *fanpos = nullptr;
-    double *fan_theta = nullptr;
-    uint8_t *fan_interior = nullptr;
+    FanHdr *fanhdr = nullptr;
+    double *anchor_wlo = nullptr;
     size_t mesh_bytes = 0;
     // workspace
     long long cap = 0;
@@ -1467,10 +1523,8 @@ static int ensure_ws(pch_mesh *m, long long cap) {
     p = Params{};
     p.face = m->face;
     p.fan = m->fan;
-    p.fan_off = m->fan_off;
-    p.fanpos = m->fanpos;
-    p.fan_theta = m->fan_theta;
-    p.fan_interior = m->fan_interior;
+    p.fanhdr = m->fanhdr;
+    p.anchor_wlo = m->anchor_wlo;
     p.nv = m->nv;
     p.nhe = m->nhe;
     if ((rc = ws_alloc(m, &p.dist_cur, m->nv))) return rc;
@@ -1716,6 +1770,19 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
     fan_off[n_vertices] = (int32_t)fan.size();
     for (int64_t j = 0; j < nhe; ++j)
         if (fanpos[j] < 0) return fail(PCH_ERR_MESH, "half-edge not reachable in its vertex fan (non-manifold vertex)");
+    std::vector<FanHdr> hdr(n_vertices);
+    std::vector<double> awlo(nhe);
+    for (int64_t v = 0; v < n_vertices; ++v) {
+        const long long m_ = fan_off[v + 1] - fan_off[v];
+        const long long meta = (long long)(uint32_t)fan_off[v] | (m_ << 32) |
+                               (interior[v] ? (long long)(1ull << 63) : 0ll);
+        hdr[v].theta = theta[v];
+        std::memcpy(&hdr[v].meta_bits, &meta, sizeof(meta));
+    }
+    for (int64_t j = 0; j < nhe; ++j) {
+        const int64_t v = origin[j];
+        awlo[j] = fan[fan_off[v] + fanpos[j]].wlo;
+    }
 
     pch_mesh *m = new pch_mesh();
     m->device = device;
@@ -1736,10 +1803,8 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
     };
     if ((e = up((void **)&m->face, face.data(), sizeof(FaceRec) * n_faces)) != cudaSuccess ||
         (e = up((void **)&m->fan, fan.data(), sizeof(FanRec) * fan.size())) != cudaSuccess ||
-        (e = up((void **)&m->fan_off, fan_off.data(), sizeof(int32_t) * fan_off.size())) != cudaSuccess ||
-        (e = up((void **)&m->fanpos, fanpos.data(), sizeof(int32_t) * nhe)) != cudaSuccess ||
-        (e = up((void **)&m->fan_theta, theta.data(), sizeof(double) * n_vertices)) != cudaSuccess ||
-        (e = up((void **)&m->fan_interior, interior.data(), n_vertices)) != cudaSuccess)
+        (e = up((void **)&m->fanhdr, hdr.data(), sizeof(FanHdr) * n_vertices)) != cudaSuccess ||
+        (e = up((void **)&m->anchor_wlo, awlo.data(), sizeof(double) * nhe)) != cudaSuccess)
         return cleanup(PCH_ERR_CUDA, std::string("mesh upload: ") + cudaGetErrorString(e));
     if ((e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreate(&m->ev0)) != cudaSuccess || (e = cudaEventCreate(&m->ev1)) != cudaSuccess ||
@@ -1763,10 +1828,8 @@ int pch_mesh_destroy(pch_mesh *m) {
     free_ws(m);
     cudaFree(m->face);
     cudaFree(m->fan);
-    cudaFree(m->fan_off);
-    cudaFree(m->fanpos);
-    cudaFree(m->fan_theta);
-    cudaFree(m->fan_interior);
+    cudaFree(m->fanhdr);
+    cudaFree(m->anchor_wlo);
     cudaFree(m->d_src);
     cudaFree(m->d_out);
     cudaFree(m->trace);

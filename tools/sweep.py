@@ -17,7 +17,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 TR = ("t0", "a_end", "b1", "b_end", "b2", "ns", "np", "nc", "nf", "ntv", "tsel", "fan_end",
-      "start_max", "work_end", "scan_end")
+      "start_max", "work_end", "scan_end", "trip0", "loaded")
 
 
 def parse(spec):
@@ -56,6 +56,13 @@ def trace_summary(path):
               f"work(t0->max work end)={np.mean(we[ok] - t0[ok])/1e3:.2f}us "
               f"scan(->max scan end)={np.mean(se[ok] - we[ok])/1e3:.2f}us "
               f"rest(->A end)={np.mean(ae[ok] - se[ok])/1e3:.2f}us", flush=True)
+        t0m, ld = a[:, 15], a[:, 16]
+        ok2 = ok & (t0m > 0) & (ld > 0)
+        if ok2.any():
+            print(f"   setup(t0->max trip0)={np.mean(t0m[ok2] - t0[ok2])/1e3:.2f}us "
+                  f"window loaded(max)={np.mean(ld[ok2] - t0[ok2])/1e3:.2f}us "
+                  f"propagate(loaded->work end)={np.mean(we[ok2] - ld[ok2])/1e3:.2f}us "
+                  f"fan warps end={np.mean(np.where(a[:, 11] > 0, a[:, 11] - t0, 0)[ok2])/1e3:.2f}us", flush=True)
 
 
 def main():

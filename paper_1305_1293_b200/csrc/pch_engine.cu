@@ -71,6 +71,7 @@ constexpr int NSLOT = 4;
 
 struct Ctrl {
     Slot slot[NSLOT];
+    unsigned long long lat_hist[64];  // PCH_PROFILE: log2 histogram of propagation cycles
     unsigned int bar_count;
     unsigned int bar_gen;
     int error;
@@ -158,7 +159,8 @@ __device__ __forceinline__ void grid_barrier(Ctrl *c, unsigned int &gen, After &
     if (threadIdx.x == 0) {
         gen += 1;
         const unsigned int target = gen * gridDim.x;
-        __threadfence();
+        // release (cumulative over the CTA's writes ordered by the
+        // __syncthreads above) / acquire pairing: no separate fences
         asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&c->bar_count), "r"(1u) : "memory");
         unsigned int spins = 0;
         unsigned long long t0 = 0;
@@ -171,7 +173,6 @@ __device__ __forceinline__ void grid_barrier(Ctrl *c, unsigned int &gen, After &
                 }
             }
         }
-        __threadfence();
         after();
     }
     __syncthreads();
@@ -250,12 +251,14 @@ __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
 
 // Run counters.  The hot ones (ST_PROPAGATED .. ST_FANS) are packed as
 // 8-bit fields into two per-thread registers and folded into the CTA's
-// shared counters once per trip (warp sum, one shared atomic per nonzero
-// field from lane 0): a shared-memory atomic per increment serialises the
-// propagation path (measured ~25% of the solve).  Per trip a thread adds
-// at most 4 to any field, so a warp's field sum stays below 256.  The
-// others (profiling clocks, maxima) and `direct` objects go straight to
-// shared memory.
+// shared counters every FOLD_TRIPS trips and at exit (one warp reduction
+// per field, one shared atomic per nonzero field from lane 0): a
+// shared-memory atomic per increment serialises the propagation path
+// (measured ~25% of the solve).  Per trip a thread adds at most 4 to any
+// field, so FOLD_TRIPS = 60 keeps every field below 256.  The others
+// (profiling clocks, maxima) and `direct` objects go straight to shared
+// memory.
+constexpr int FOLD_TRIPS = 60;
 struct LocalStats {
     unsigned long long *s;
     bool direct;
@@ -270,25 +273,20 @@ struct LocalStats {
         }
     }
     __device__ __forceinline__ void max(int i, unsigned long long x) { atomicMax(s + i, x); }
-    // fold the packed fields into shared memory (whole warp, converged)
+    // fold the packed fields into shared memory (whole warp, converged):
+    // one warp reduction per field, lane 0 adds the nonzero sums
     __device__ __forceinline__ void fold() {
-        unsigned long long x = a, y = b;
+        const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            x += __shfl_xor_sync(0xffffffffu, x, o);
-            y += __shfl_xor_sync(0xffffffffu, y, o);
+        for (int k = 0; k <= ST_STORED; ++k) {
+            const unsigned int f = __reduce_add_sync(0xffffffffu, (unsigned int)((a >> (8 * k)) & 0xffull));
+            if (lane == 0 && f) atomicAdd(s + k, (unsigned long long)f);
         }
-        if ((threadIdx.x & 31) == 0) {
 #pragma unroll
-            for (int k = 0; k <= ST_STORED; ++k) {
-                unsigned long long f = (x >> (8 * k)) & 0xffull;
-                if (f) atomicAdd(s + k, f);
-            }
-#pragma unroll
-            for (int k = ST_EV_CREATED; k <= ST_FANS; ++k) {
-                unsigned long long f = (y >> (8 * (k - ST_EV_CREATED))) & 0xffull;
-                if (f) atomicAdd(s + k, f);
-            }
+        for (int k = ST_EV_CREATED; k <= ST_FANS; ++k) {
+            const unsigned int f =
+                __reduce_add_sync(0xffffffffu, (unsigned int)((b >> (8 * (k - ST_EV_CREATED))) & 0xffull));
+            if (lane == 0 && f) atomicAdd(s + k, (unsigned long long)f);
         }
         a = b = 0ull;
     }
@@ -325,6 +323,7 @@ __device__ __forceinline__ void flush_stats(Ctrl *c, unsigned long long *s) {
 #endif
 constexpr int TPB = PCH_TPB;      // threads per CTA of every solver kernel
 constexpr int NWARP = TPB / 32;
+constexpr double DELTA_FLOOR = 0.15;  // controller step floor, mean edge lengths
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
@@ -634,7 +633,8 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
         // endpoint inequalities of the ICH filter (paper Fig. 4b) against
         // the current field: paths through v0 (resp. v1) already reach the
         // far end of the interval more cheaply -> the window is useless
-        const double tB = dps + hyp(ix - b1, iy), tA = dps + hyp(ix - b0, iy);
+        // |I B| = d1 and |I A| = d0 by construction of I
+        const double tB = dps + d1, tA = dps + d0;
         if ((tB > g0 + b1 + EPS_NUM) || (tA > g1 + (ell - b0) + EPS_NUM)) {
             ls.add(ST_RECHECK);
             return 0;
@@ -654,14 +654,18 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     const double dy = dy2 > 0.0 ? -sqrt(dy2) : 0.0;
     const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
     const double vdx = dx - ix, vdy = dy - iy;
-    const double nvd = hyp(vdx, vdy);
+    const double nvd2 = vdx * vdx + vdy * vdy;
+    const double nvd = sqrt(nvd2);
     const double ca = uax * vdy - uay * vdx;
     const double cb = ubx * vdy - uby * vdx;
-    const double tola = EPS_NUM * hyp(uax, uay) * nvd;
-    const double tolb = EPS_NUM * hyp(ubx, uby) * nvd;
+    // tolerances EPS_NUM |IA| |ID| and EPS_NUM |IB| |ID| compared squared
+    // (|IA| = d0, |IB| = d1 up to the unfold's rounding; geom.py:408-409)
+    const double e2 = EPS_NUM * EPS_NUM * nvd2;
+    const bool a_in = ca > 0.0 && ca * ca > e2 * (uax * uax + uay * uay);
+    const bool b_out = cb < 0.0 && cb * cb > e2 * (ubx * ubx + uby * uby);
     // occ: the ray to the apex passes strictly inside (A, B) -- w occupies vd
-    const bool occ = far && ca > tola && cb < -tolb;
-    const bool left = cb >= -tolb;  // (not occ) both rays exit through edge v0-D
+    const bool occ = far && a_in && b_out;
+    const bool left = !b_out;  // (not occ) both rays exit through edge v0-D
     const double comp = dps + nvd;
     const double denom = iy - dy;
     const double entry_x = denom > 1e-300 ? ix + (dx - ix) * (iy / denom) : ix;
@@ -1127,6 +1131,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
     LocalStats ls{s_st, false};   // packed per-thread counters, folded per trip
     LocalStats lsd{s_st, true};   // rare paths: straight to shared memory
     int maxchild = 0;
+    int trips_since_fold = 0;
     const unsigned long long gthreads = (unsigned long long)gridDim.x * TPB;
     const unsigned long long nwarps = gthreads >> 5;
     const unsigned long long gwid = (unsigned long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
@@ -1236,9 +1241,20 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                         asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
                         atomicMax(&s_tl, globaltimer());
                     }
+                    long long c1 = 0;
+                    if (p.prof) {
+                        asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
+                        c1 = clock64();
+                    }
                     no = propagate(p, sg, it, &cur.nF, p.fanev[it & 1], win, o0, o1, ls);
                     if (no > maxchild) maxchild = no;
-                    if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
+                    if (p.prof) {
+                        asm volatile("" ::"d"((no > 0 ? o0.key : 0.0) + (no > 1 ? o1.key : 0.0)));
+                        const long long c2p = clock64();
+                        ls.add(ST_CYC_PROP, c2p - c0);
+                        const unsigned long long dtp = (unsigned long long)(c2p - c1);
+                        atomicAdd(&ctrl->lat_hist[63 - __clzll(dtp | 1ull)], 1ull);
+                    }
                 }
             } else if (wi < nwS + nwF) {
                 // FANS_PER_WARP candidates per warp, FAN_LANES lanes each
@@ -1329,7 +1345,10 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 if ((long long)at < p.fancap) fout[at] = sg.fe[k];
                 else atomicExch(&ctrl->error, ERR_OVERFLOW);
             }
-            ls.fold();
+            if (++trips_since_fold == FOLD_TRIPS) {
+                ls.fold();
+                trips_since_fold = 0;
+            }
             __syncthreads();
             if (threadIdx.x == 0) sg.nfe = 0u;
             __syncthreads();
@@ -1370,6 +1389,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
         if (err || (ns == 0 && np == 0 && nf == 0)) break;
         t = tn;
     }
+    ls.fold();
     if (maxchild) ls.max(ST_MAXCHILD, maxchild);
     flush_stats(ctrl, s_st);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1577,9 +1597,21 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.fan_full = cfg->fan_mode == 1;
         p.recheck = (cfg->flags & PCH_FLAG_NO_RECHECK) ? 0 : 1;
         p.live = (cfg->flags & PCH_FLAG_DETERMINISTIC) ? 0 : 1;
+        // step controller bounds (mean edge lengths): the floor keeps wide
+        // wavefronts (tori, large spheres: far more than k windows per face
+        // layer) from splitting one layer over many iterations; measured
+        // best compromise over the bench meshes (profiles/r01_controller.md)
         p.delta0 = m->mean_edge;
-        p.delta_min = 1e-3 * m->mean_edge;
+        p.delta_min = DELTA_FLOOR * m->mean_edge;
         p.delta_max = 1e3 * m->mean_edge;
+        if (const char *fd = getenv("PCH_DELTA")) {  // development: fixed step
+            const double dlt = atof(fd) * m->mean_edge;
+            if (dlt > 0.0) p.delta0 = p.delta_min = p.delta_max = dlt;
+        }
+        if (const char *fm = getenv("PCH_DELTA_MIN")) {  // development: step floor
+            const double dlt = atof(fm) * m->mean_edge;
+            if (dlt > 0.0) p.delta_min = dlt;
+        }
         p.prof = getenv("PCH_PROFILE") ? 1 : 0;
         const char *trace_path = getenv("PCH_TRACE");
         if (trace_path && !m->trace) {
@@ -1623,6 +1655,10 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             }
         }
         if (p.prof) {
+            fprintf(stderr, "PCH_PROFILE propagation latency log2(cycles) histogram:");
+            for (int b = 0; b < 64; ++b)
+                if (c.lat_hist[b]) fprintf(stderr, " [2^%d]=%llu", b, c.lat_hist[b]);
+            fprintf(stderr, "\n");
             const unsigned long long *q = c.st;
             fprintf(stderr, "PCH_PROFILE prop sections cycles/propagation: window %.0f face+split %.0f "
                     "dist %.0f unfold+recheck %.0f children %.0f events %.0f\n",

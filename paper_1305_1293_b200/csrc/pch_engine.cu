@@ -688,8 +688,13 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     Win cl, cr;
     const int fl = make_child(3 * (fr / 3) + a1, cho_l, lan, 0.0, 0.0, dx, dy, rA, occ ? 1.0 : rB,
                               ix, iy, dps, g0, gdd, g1, ell, 0.0, true, p.eps_win, cl);
+#ifdef PCH_EXP_ONECHILD
+    const int frr = CH_TINY;
+    cr = cl;
+#else
     const int frr = make_child(3 * (fr / 3) + a2, cho_r, lpv, dx, dy, ell, 0.0, occ ? 0.0 : rA, rB,
                                ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, cr);
+#endif
     const bool ml = want_l && okL, mr = want_r && okR;  // children computed
     const bool sl = ml && fl == CH_STORED, sr = mr && frr == CH_STORED;
     // accounting as the reference counts it (geom.py:433-516)

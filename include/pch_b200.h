@@ -56,7 +56,11 @@ typedef struct pch_config {
     int64_t max_iterations;  /* <= 0: no cap */
     int64_t pool_capacity;   /* initial window-pool capacity; 0 = auto */
     int32_t flags;           /* PCH_FLAG_* */
-    int32_t reserved;
+    int32_t chain;           /* propagations one thread may chain per
+                                iteration: a child the next batch would
+                                select is propagated at once by the same
+                                thread (0 = library default 2, 1 = off;
+                                one-barrier solver only) */
 } pch_config;
 
 #define PCH_FLAG_NO_RECHECK 1   /* disable the pop-time endpoint re-check */

@@ -35,7 +35,7 @@ class PchConfig(ctypes.Structure):
                 ("fan_mode", ctypes.c_int32), ("epsilon_window", ctypes.c_double),
                 ("max_iterations", ctypes.c_int64),
                 ("pool_capacity", ctypes.c_int64), ("flags", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("chain", ctypes.c_int32)]
 
 
 STAT_FIELDS = ("iterations", "windows_propagated", "total_windows_created",

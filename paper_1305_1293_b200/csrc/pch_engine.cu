@@ -117,6 +117,7 @@ struct Params {
     int recheck;
     int live;                  // filters read the live shadow tables
     int prof;                  // PCH_PROFILE: accumulate per-section clocks
+    int chain;                 // max propagations a thread chains per iteration
     unsigned long long *trace; // optional per-iteration timeline (TR_* records)
     long long trace_cap;       // iterations the trace buffer holds
 };
@@ -324,6 +325,7 @@ __device__ __forceinline__ void flush_stats(Ctrl *c, unsigned long long *s) {
 constexpr int TPB = PCH_TPB;      // threads per CTA of every solver kernel
 constexpr int NWARP = TPB / 32;
 constexpr double DELTA_FLOOR = 0.15;  // controller step floor, mean edge lengths
+constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
@@ -1251,8 +1253,21 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                         asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
                         c1 = clock64();
                     }
-                    no = propagate(p, sg, it, &cur.nF, p.fanev[it & 1], win, o0, o1, ls);
-                    if (no > maxchild) maxchild = no;
+                    // chaining: a child that the next batch would select
+                    // (key <= t_{i+1}) is propagated right away by the same
+                    // thread, up to p.chain propagations; its sibling is
+                    // routed directly
+                    for (int step = 1;; ++step) {
+                        no = propagate(p, sg, it, &cur.nF, p.fanev[it & 1], win, o0, o1, ls);
+                        if (no > maxchild) maxchild = no;
+                        if (step >= p.chain || no == 0) break;
+                        const bool c0ok = o0.key <= tn, c1ok = no > 1 && o1.key <= tn;
+                        if (!c0ok && !c1ok) break;
+                        const bool take1 = c1ok && (!c0ok || o1.key < o0.key);
+                        if (no > 1) put_direct(take1 ? o0 : o1);
+                        win = take1 ? o1 : o0;
+                        no = 0;
+                    }
                     if (p.prof) {
                         asm volatile("" ::"d"((no > 0 ? o0.key : 0.0) + (no > 1 ? o1.key : 0.0)));
                         const long long c2p = clock64();
@@ -1586,6 +1601,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
     if (cfg->k < 1) return fail(PCH_ERR_CONFIG, "k must be >= 1");
     if (!(cfg->epsilon_window > 0.0)) return fail(PCH_ERR_CONFIG, "epsilon_window must be > 0");
     if (cfg->fan_mode != 0 && cfg->fan_mode != 1) return fail(PCH_ERR_CONFIG, "fan_mode must be clip or full_edges");
+    if (cfg->chain < 0) return fail(PCH_ERR_CONFIG, "chain must be >= 0");
     long long cap = cfg->pool_capacity > 0 ? cfg->pool_capacity
                                            : std::max<long long>(1 << 20, 2ll * m->nhe);
     if (m->cap > cap) cap = m->cap;
@@ -1618,6 +1634,8 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             if (dlt > 0.0) p.delta_min = dlt;
         }
         p.prof = getenv("PCH_PROFILE") ? 1 : 0;
+        p.chain = cfg->chain > 0 ? cfg->chain : DEFAULT_CHAIN;
+        if (const char *ch = getenv("PCH_CHAIN")) p.chain = std::max(1, atoi(ch));  // development
         const char *trace_path = getenv("PCH_TRACE");
         if (trace_path && !m->trace) {
             m->trace_cap = 1 << 17;

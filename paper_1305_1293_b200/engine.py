@@ -50,6 +50,10 @@ class EngineConfig:
     update): fields are then bitwise identical across runs.  The default
     one-barrier solver reads the live tables and is faster; its fields
     agree across runs to rounding (far inside the 1e-9 bar).
+    ``chain`` bounds how many propagations one thread performs per
+    iteration when a child falls inside the next batch's threshold (it is
+    then propagated at once instead of waiting for the next iteration);
+    0 = library default (2), 1 = off.
     """
 
     k: int = 16384
@@ -63,6 +67,7 @@ class EngineConfig:
     recheck: bool = True
     pool_capacity: int = 0
     deterministic: bool = False
+    chain: int = 0
 
     def __post_init__(self):
         if self.k < 1:
@@ -75,6 +80,8 @@ class EngineConfig:
             raise ValueError(f"fan_mode must be one of {FAN_MODES}")
         if not self.epsilon_window > 0.0:
             raise ValueError("epsilon_window must be > 0")
+        if self.chain < 0:
+            raise ValueError("chain must be >= 0")
 
     def to_native(self) -> _native.PchConfig:
         c = _native.PchConfig()
@@ -86,6 +93,7 @@ class EngineConfig:
         c.pool_capacity = int(self.pool_capacity)
         c.flags = ((0 if self.recheck else _native.FLAG_NO_RECHECK)
                    | (_native.FLAG_DETERMINISTIC if self.deterministic else 0))
+        c.chain = int(self.chain)
         return c
 
 

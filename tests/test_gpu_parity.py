@@ -86,6 +86,16 @@ def test_fan_mode_full_edges_matches():
     assert max_rel_dev(d, g["ich_dist"]) <= TOL
 
 
+@pytest.mark.parametrize("chain", [1, 2, 4])
+def test_chain_lengths_match(chain):
+    _gpu()
+    from paper_1305_1293_b200 import EngineConfig, run_pch
+    for name in ("bumpy_sphere20k_s3", "bumpy_torus4800_s5", "icosphere5120_multi16"):
+        m, g = load_golden(name)
+        d, _ = run_pch(m, g["sources"], EngineConfig(chain=chain))
+        assert max_rel_dev(d, g["ich_dist"]) <= TOL, (name, chain)
+
+
 def test_recheck_off_matches():
     _gpu()
     from paper_1305_1293_b200 import EngineConfig, run_pch

@@ -61,8 +61,12 @@ def test_engine_config_validation():
         EngineConfig(selection_mode="sorted")
     with pytest.raises(ValueError):
         EngineConfig(fan_mode="none")
-    c = EngineConfig(k=123, fan_mode="full_edges", recheck=False).to_native()
-    assert (c.k, c.fan_mode, c.flags) == (123, 1, _native.FLAG_NO_RECHECK)
+    with pytest.raises(ValueError):
+        EngineConfig(chain=-1)
+    c = EngineConfig(k=123, fan_mode="full_edges", recheck=False, chain=3).to_native()
+    assert (c.k, c.fan_mode, c.flags, c.chain) == (123, 1, _native.FLAG_NO_RECHECK, 3)
+    c = EngineConfig(deterministic=True).to_native()
+    assert c.flags == _native.FLAG_DETERMINISTIC
 
 
 def test_source_validation_matches_reference(cube):

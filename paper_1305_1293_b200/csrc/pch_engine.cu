@@ -382,7 +382,7 @@ __device__ __forceinline__ void fan_event(const Params &p, Stage &sg, int it, un
     // never does (a new candidate is always strictly smaller) and seeds the
     // CAS with the pick it read, so a claim is one round trip.
     const unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
-    const unsigned long long lo = ((unsigned long long)(uint32_t)anchor << 32) | ord_hi32(fan_rel(e));
+    const unsigned long long lo = fan_tiebreak(e);
     cas_min_u128(p.fanpick[p.live ? 0 : it % 3] + v, hi, lo, guess);
     const unsigned int k = atomicAdd(&sg.nfe, 1u);
     if (k < (unsigned int)FE_CAP) {
@@ -969,7 +969,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                     const double dv = __ldcg(p.dist_cur + e.v);
                     const ulonglong2 pk = __ldcg(p.fanpick[(it + 2) % 3] + e.v);
                     const unsigned long long lo =
-                        ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(rel);
+                        fan_tiebreak(e);
                     FanSpan f;
                     if (__double_as_longlong(dv) == __double_as_longlong(e.cand) &&
                         pk.x == (unsigned long long)__double_as_longlong(e.cand) && pk.y == lo &&
@@ -1287,7 +1287,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                     const ulonglong2 pk = __ldcg(p.fanpick[0] + e.v);
                     const double rel = fan_rel(e);
                     const unsigned long long hi = (unsigned long long)__double_as_longlong(e.cand);
-                    const unsigned long long lo = ((unsigned long long)(uint32_t)e.anchor << 32) | ord_hi32(rel);
+                    const unsigned long long lo = fan_tiebreak(e);
                     // the fan's span is read speculatively, in parallel with
                     // the winner check: the winner of the vertex's pick,
                     // still at the vertex's distance (a later improvement

@@ -53,7 +53,7 @@ enum { ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_PRUNE_TINY,
        // PCH_PROFILE section clocks (clock64 deltas summed over threads)
        ST_CYC_LOAD, ST_CYC_PROP, ST_CYC_EVENTS, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
        ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CYC_P1, ST_CYC_P2, ST_CYC_P3, ST_CYC_P4,
-       ST_CYC_P5, N_ST };
+       ST_CYC_P5, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES, N_ST };
 
 enum { ERR_NONE = 0, ERR_OVERFLOW = 1, ERR_GUARD = 2, ERR_TIMEOUT = 3 };
 
@@ -227,7 +227,8 @@ __device__ __forceinline__ int key_bin(double key, double base, double w) {
 }
 
 __device__ __forceinline__ void store_win(const WinSoA &W, unsigned long long i, const Win &c) {
-    W.hj[i] = make_int2(c.he, c.jo);
+    W.hv[i] = make_int4(c.he, c.jo, (int)c.v0f, (int)c.v1f);
+    W.vd[i] = c.vdf;
     W.b0[i] = c.b0;
     W.b1[i] = c.b1;
     W.d0[i] = c.d0;
@@ -238,9 +239,12 @@ __device__ __forceinline__ void store_win(const WinSoA &W, unsigned long long i,
 
 __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
     Win c;
-    const int2 hj = __ldcg(W.hj + i);
-    c.he = hj.x;
-    c.jo = hj.y;
+    const int4 hv = __ldcg(W.hv + i);
+    c.he = hv.x;
+    c.jo = hv.y;
+    c.v0f = (uint32_t)hv.z;
+    c.v1f = (uint32_t)hv.w;
+    c.vdf = __ldcg(W.vd + i);
     c.b0 = __ldcg(W.b0 + i);
     c.b1 = __ldcg(W.b1 + i);
     c.d0 = __ldcg(W.d0 + i);
@@ -354,7 +358,13 @@ __device__ __forceinline__ void dist_event(const Params &p, Stage &sg, int32_t v
 __device__ __forceinline__ void angle_event(const Params &p, Stage &sg, int32_t j, double comp,
                                             double entry, ulonglong2 guess, LocalStats &ls) {
     ls.add(ST_EV_CREATED);
-    if (cas_min_u128(p.split_new + j, ord64(comp), ord64(entry), guess)) {
+    int tries = 0;
+    const bool won = cas_min_u128(p.split_new + j, ord64(comp), ord64(entry), guess, &tries);
+    if (p.prof) {
+        atomicAdd(&p.ctrl->st[ST_CAS_ANGLE_CALLS], 1ull);
+        atomicAdd(&p.ctrl->st[ST_CAS_ANGLE_TRIES], (unsigned long long)tries);
+    }
+    if (won) {
         if (!p.live) {
             unsigned int k = atomicAdd(&sg.nte, 1u);
             sg.te[k] = j;
@@ -383,7 +393,12 @@ __device__ __forceinline__ void fan_event(const Params &p, Stage &sg, int it, un
     // CAS with the pick it read, so a claim is one round trip.
     const unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
     const unsigned long long lo = fan_tiebreak(e);
-    cas_min_u128(p.fanpick[p.live ? 0 : it % 3] + v, hi, lo, guess);
+    int tries = 0;
+    cas_min_u128(p.fanpick[p.live ? 0 : it % 3] + v, hi, lo, guess, &tries);
+    if (p.prof) {
+        atomicAdd(&p.ctrl->st[ST_CAS_FAN_CALLS], 1ull);
+        atomicAdd(&p.ctrl->st[ST_CAS_FAN_TRIES], (unsigned long long)tries);
+    }
     const unsigned int k = atomicAdd(&sg.nfe, 1u);
     if (k < (unsigned int)FE_CAP) {
         sg.fe[k] = e;
@@ -546,6 +561,9 @@ __device__ __forceinline__ void fan_item(const Params &p, double cand, const Fan
         return;
     }
     int32_t pid = __ldg(&fr.pid), qid = __ldg(&fr.qid);
+    const uint32_t sad = __ldg(&fr.sad);
+    const uint32_t cv0 = (uint32_t)pid | ((sad & 1u) ? SADDLE_BIT : 0u);
+    const uint32_t cv1 = (uint32_t)qid | ((sad & 2u) ? SADDLE_BIT : 0u);
     double gp, gq;
     if (fresh) {
         gp = __longlong_as_double((long long)__ldcg(p.dist_new + pid));
@@ -555,7 +573,8 @@ __device__ __forceinline__ void fan_item(const Params &p, double cand, const Fan
         gq = gdist(p, qid);
     }
     Win c;
-    int fate = make_child(__ldg(&fr.che), __ldg(&fr.cho), __ldg(&fr.lc), px, py, qx, qy, s0, s1, 0.0, 0.0, cand,
+    int fate = make_child(__ldg(&fr.che), __ldg(&fr.cho), cv0, cv1, __ldg(&fr.capx), __ldg(&fr.lc), px, py,
+                          qx, qy, s0, s1, 0.0, 0.0, cand,
                           gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, c);
     if (fate == CH_STORED) {
         emit(c);
@@ -608,10 +627,11 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     const double ell = __ldg(&fp->len[a]);
     const double lan = __ldg(&fp->len[a1]);
     const double lpv = __ldg(&fp->len[a2]);
-    const uint32_t va = __ldg(&fp->vid[a]), vb = __ldg(&fp->vid[a1]);
-    const uint32_t v0f = far ? vb : va, v1f = far ? va : vb;
-    const uint32_t vdf = __ldg(&fp->vid[a2]);
+    // the window's vertices (carried from its creation): the distances
+    // below are issued together with the face record
+    const uint32_t v0f = w.v0f, v1f = w.v1f, vdf = far ? w.vdf : 0u;
     const int32_t cho_l = __ldg(&fp->opp[a1]), cho_r = __ldg(&fp->opp[a2]);
+    const uint32_t apx_l = __ldg(&fp->apx[a1]), apx_r = __ldg(&fp->apx[a2]);
     ulonglong2 sp_raw = make_ulonglong2(0ull, 0ull);
     const double2 sp = far ? gsplit(p, j, sp_raw) : make_double2(INFINITY, 0.0);
     // level 2: distances at the three vertices
@@ -687,16 +707,16 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     const bool okB = ray_seg(ix, iy, b1, 0.0, eB_left ? 0.0 : dx, eB_left ? 0.0 : dy,
                              eB_left ? dx : ell, eB_left ? dy : 0.0, rB);
     const bool okL = okA && (occ || okB), okR = okB && (occ || okA);
+    const double candd = comp;
+    const bool evd = occ && candd < gdd;
+    int nc = 0;
     Win cl, cr;
-    const int fl = make_child(3 * (fr / 3) + a1, cho_l, lan, 0.0, 0.0, dx, dy, rA, occ ? 1.0 : rB,
+    const int fl = make_child(3 * (fr / 3) + a1, cho_l, v0f, vdf, apx_l, lan, 0.0, 0.0, dx, dy, rA,
+                              occ ? 1.0 : rB,
                               ix, iy, dps, g0, gdd, g1, ell, 0.0, true, p.eps_win, cl);
-#ifdef PCH_EXP_ONECHILD
-    const int frr = CH_TINY;
-    cr = cl;
-#else
-    const int frr = make_child(3 * (fr / 3) + a2, cho_r, lpv, dx, dy, ell, 0.0, occ ? 0.0 : rA, rB,
+    const int frr = make_child(3 * (fr / 3) + a2, cho_r, vdf, v1f, apx_r, lpv, dx, dy, ell, 0.0,
+                               occ ? 0.0 : rA, rB,
                                ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, cr);
-#endif
     const bool ml = want_l && okL, mr = want_r && okR;  // children computed
     const bool sl = ml && fl == CH_STORED, sr = mr && frr == CH_STORED;
     // accounting as the reference counts it (geom.py:433-516)
@@ -707,7 +727,6 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     ls.add(ST_PRUNE_DEGEN, degen + (ml && fl == CH_DEGEN ? 1u : 0u) + (mr && frr == CH_DEGEN ? 1u : 0u));
     ls.add(ST_PRUNE_TINY, (ml && fl == CH_TINY ? 1u : 0u) + (mr && frr == CH_TINY ? 1u : 0u));
     ls.add(ST_PRUNE_ICH, (ml && fl == CH_ICH ? 1u : 0u) + (mr && frr == CH_ICH ? 1u : 0u));
-    int nc = 0;
     if (sl) {
         out0 = cl;
         nc = 1;
@@ -717,8 +736,6 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
         else out0 = cr;
         ++nc;
     }
-    const double candd = comp;
-    const bool evd = occ && candd < gdd;
 
     // ---- events, issued together (order independent: min / CAS-min) ----
     if (ev0) dist_event(p, sg, v0, cand0, ls);
@@ -1545,7 +1562,8 @@ static int ws_alloc(pch_mesh *m, T **out, size_t count) {
 
 static int alloc_soa(pch_mesh *m, WinSoA &W, long long cap) {
     int rc;
-    if ((rc = ws_alloc(m, &W.hj, cap))) return rc;
+    if ((rc = ws_alloc(m, &W.hv, cap))) return rc;
+    if ((rc = ws_alloc(m, &W.vd, cap))) return rc;
     if ((rc = ws_alloc(m, &W.b0, cap))) return rc;
     if ((rc = ws_alloc(m, &W.b1, cap))) return rc;
     if ((rc = ws_alloc(m, &W.d0, cap))) return rc;
@@ -1678,6 +1696,9 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             }
         }
         if (p.prof) {
+            fprintf(stderr, "PCH_PROFILE CAS: angle %llu calls %llu tries, fan %llu calls %llu tries\n",
+                    c.st[ST_CAS_ANGLE_CALLS], c.st[ST_CAS_ANGLE_TRIES], c.st[ST_CAS_FAN_CALLS],
+                    c.st[ST_CAS_FAN_TRIES]);
             fprintf(stderr, "PCH_PROFILE propagation latency log2(cycles) histogram:");
             for (int b = 0; b < 64; ++b)
                 if (c.lat_hist[b]) fprintf(stderr, " [2^%d]=%llu", b, c.lat_hist[b]);
@@ -1780,6 +1801,7 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
             r.len[a] = length[j];
             r.vid[a] = vflag(origin[j]);
             r.opp[a] = (int32_t)opposite[j];
+            r.apx[a] = opposite[j] >= 0 ? vflag(origin[prv_he(opposite[j])]) : 0u;
         }
     }
     // fan tables: for every vertex walk its outgoing half-edges
@@ -1811,8 +1833,10 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
             f.lc = length[che];
             f.che = (int32_t)che;
             f.cho = (int32_t)opposite[che];
+            f.capx = opposite[che] >= 0 ? vflag(origin[prv_he(opposite[che])]) : 0u;
             f.pid = (int32_t)origin[che];
             f.qid = (int32_t)origin[hprev];
+            f.sad = (vertex_class[origin[che]] == 2 ? 1u : 0u) | (vertex_class[origin[hprev]] == 2 ? 2u : 0u);
             fanpos[h] = (int32_t)(fan.size() - fan_off[v]);
             fan.push_back(f);
             int64_t o = opposite[hprev];

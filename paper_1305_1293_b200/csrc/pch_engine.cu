@@ -1254,8 +1254,9 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
         if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_TRIP0);
         for (unsigned int tr = 0; tr < trips; ++tr) {
             const unsigned long long wi = tr * nwarps + gwid;
-            Win o0, o1;
+            Win o0, o1, o2;   // o2: a sibling left behind by chaining
             int no = 0;
+            bool h2 = false;
             if (wi < nwS) {
                 const unsigned long long i = (wi << 5) + lane;
                 if (i < nS) {
@@ -1281,7 +1282,16 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                         const bool c0ok = o0.key <= tn, c1ok = no > 1 && o1.key <= tn;
                         if (!c0ok && !c1ok) break;
                         const bool take1 = c1ok && (!c0ok || o1.key < o0.key);
-                        if (no > 1) put_direct(take1 ? o0 : o1);
+                        if (no > 1) {
+                            // the child not chained: routed with the trip's
+                            // scan (first one) or directly (chain > 2)
+                            if (!h2) {
+                                o2 = take1 ? o0 : o1;
+                                h2 = true;
+                            } else {
+                                put_direct(take1 ? o0 : o1);
+                            }
+                        }
                         win = take1 ? o1 : o0;
                         no = 0;
                     }
@@ -1343,12 +1353,15 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
             long long c2 = p.prof ? clock64() : 0;
             const bool s0 = no > 0 && o0.key <= tn, s1 = no > 1 && o1.key <= tn;
             const bool k0 = no > 0 && !s0, k1 = no > 1 && !s1;
-            const unsigned int ns_ = (unsigned int)s0 + (unsigned int)s1;
-            const unsigned int np_ = (unsigned int)k0 + (unsigned int)k1;
+            const bool s2 = h2 && o2.key <= tn, k2 = h2 && !s2;
+            const unsigned int ns_ = (unsigned int)s0 + (unsigned int)s1 + (unsigned int)s2;
+            const unsigned int np_ = (unsigned int)k0 + (unsigned int)k1 + (unsigned int)k2;
             if (k0) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o0.key));
             if (k1) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o1.key));
+            if (k2) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o2.key));
             if (s0) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o0.key));
             if (s1) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o1.key));
+            if (s2) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o2.key));
             unsigned int tot;
             const unsigned int ex = block_excl_scan(ns_ | (np_ << 16), tot);
             if (threadIdx.x == 0) {
@@ -1372,8 +1385,12 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 else put(Pn, pa++, o0);
             }
             if (no > 1) {
-                if (s1) put(Sn, sa, o1);
-                else put(Pn, pa, o1);
+                if (s1) put(Sn, sa++, o1);
+                else put(Pn, pa++, o1);
+            }
+            if (h2) {
+                if (s2) put(Sn, sa, o2);
+                else put(Pn, pa, o2);
             }
             const unsigned int nfe = min(sg.nfe, (unsigned int)FE_CAP);
             FanEv *fout = p.fanev[it & 1];

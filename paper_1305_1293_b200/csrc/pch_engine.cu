@@ -118,6 +118,7 @@ struct Params {
     int live;                  // filters read the live shadow tables
     int prof;                  // PCH_PROFILE: accumulate per-section clocks
     int chain;                 // max propagations a thread chains per iteration
+    int rows;                  // distance fields solved together (batched rows)
     unsigned long long *trace; // optional per-iteration timeline (TR_* records)
     long long trace_cap;       // iterations the trace buffer holds
 };
@@ -197,19 +198,37 @@ __device__ __forceinline__ unsigned long long warp_alloc(unsigned long long *cou
     return base + __popc(b & ((1u << lane) - 1u));
 }
 
-// distance / angle-split reads of the filters: the iteration-frozen copy,
-// or (PCH_FLAG_LIVE) the shadow tables the events update atomically.  Any
-// value read is the length of a real path, so a stale or racing read only
-// weakens pruning; it never admits a wrong distance.
-__device__ __forceinline__ double gdist(const Params &p, int32_t v) {
-    if (p.live) return __longlong_as_double((long long)__ldcg(p.dist_new + v));
+// The tables of one distance field.  Batched rows (pch_run_rows) solve R
+// independent single-source fields in one kernel: every window carries its
+// field's row, and the distance field / angle-split table / fan picks of
+// row r live at offset r * (V or 3F) -- the mesh is shared.
+struct RowTabs {
+    unsigned long long *dist;  // fp64 bit patterns (live shadow field)
+    ulonglong2 *split;         // (ord(comp), ord(entry_x))
+    ulonglong2 *pick;          // fan picks
+};
+
+__device__ __forceinline__ RowTabs row_tabs(const Params &p, uint32_t r, int it) {
+    RowTabs t;
+    t.dist = p.dist_new + (size_t)r * p.nv;
+    t.split = p.split_new + (size_t)r * p.nhe;
+    t.pick = p.fanpick[p.live ? 0 : it % 3] + (size_t)r * p.nv;
+    return t;
+}
+
+// distance / angle-split reads of the filters: the iteration-frozen copy
+// (deterministic solver, one row), or the shadow tables the events update
+// atomically.  Any value read is the length of a real path, so a stale or
+// racing read only weakens pruning; it never admits a wrong distance.
+__device__ __forceinline__ double gdist(const Params &p, const RowTabs &t, int32_t v) {
+    if (p.live) return __longlong_as_double((long long)__ldcg(t.dist + v));
     return __ldcg(p.dist_cur + v);
 }
-__device__ __forceinline__ double2 gsplit(const Params &p, int32_t j, ulonglong2 &raw) {
+__device__ __forceinline__ double2 gsplit(const Params &p, const RowTabs &t, int32_t j, ulonglong2 &raw) {
     if (p.live) {
         // 128-bit atomic read (the compare value never matches: ord64 of a
         // comparison distance always has its top bit set)
-        raw = atomicCAS(p.split_new + j, make_ulonglong2(0ull, 0ull), make_ulonglong2(0ull, 0ull));
+        raw = atomicCAS(t.split + j, make_ulonglong2(0ull, 0ull), make_ulonglong2(0ull, 0ull));
         return make_double2(unord64(raw.x), unord64(raw.y));
     }
     double2 s = __ldcg(p.split_cur + j);
@@ -228,7 +247,7 @@ __device__ __forceinline__ int key_bin(double key, double base, double w) {
 
 __device__ __forceinline__ void store_win(const WinSoA &W, unsigned long long i, const Win &c) {
     W.hv[i] = make_int4(c.he, c.jo, (int)c.v0f, (int)c.v1f);
-    W.vd[i] = c.vdf;
+    W.vr[i] = make_uint2(c.vdf, c.row);
     W.b0[i] = c.b0;
     W.b1[i] = c.b1;
     W.d0[i] = c.d0;
@@ -244,7 +263,9 @@ __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
     c.jo = hv.y;
     c.v0f = (uint32_t)hv.z;
     c.v1f = (uint32_t)hv.w;
-    c.vdf = __ldcg(W.vd + i);
+    const uint2 vr = __ldcg(W.vr + i);
+    c.vdf = vr.x;
+    c.row = vr.y;
     c.b0 = __ldcg(W.b0 + i);
     c.b1 = __ldcg(W.b1 + i);
     c.d0 = __ldcg(W.d0 + i);
@@ -330,6 +351,7 @@ constexpr int TPB = PCH_TPB;      // threads per CTA of every solver kernel
 constexpr int NWARP = TPB / 32;
 constexpr double DELTA_FLOOR = 0.15;  // controller step floor, mean edge lengths
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
+constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
@@ -342,12 +364,12 @@ struct Stage {
     FanEv fe[FE_CAP];     // saddle fan candidates (overflow appends directly)
 };
 
-__device__ __forceinline__ void dist_event(const Params &p, Stage &sg, int32_t v, double cand,
-                                           LocalStats &ls) {
+__device__ __forceinline__ void dist_event(const Params &p, const RowTabs &t, Stage &sg, int32_t v,
+                                           double cand, LocalStats &ls) {
     // the caller checked cand against the distance it read; the minimum
     // itself needs no reply (RED), the vertex is listed for the commit
     ls.add(ST_EV_CREATED);
-    atomicMin(p.dist_new + v, (unsigned long long)__double_as_longlong(cand));
+    atomicMin(t.dist + v, (unsigned long long)__double_as_longlong(cand));
     if (!p.live) {
         unsigned int k = atomicAdd(&sg.ntv, 1u);
         sg.tv[k] = v;
@@ -355,11 +377,11 @@ __device__ __forceinline__ void dist_event(const Params &p, Stage &sg, int32_t v
     ls.add(ST_EV_APPLIED);
 }
 
-__device__ __forceinline__ void angle_event(const Params &p, Stage &sg, int32_t j, double comp,
-                                            double entry, ulonglong2 guess, LocalStats &ls) {
+__device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, Stage &sg, int32_t j,
+                                            double comp, double entry, ulonglong2 guess, LocalStats &ls) {
     ls.add(ST_EV_CREATED);
     int tries = 0;
-    const bool won = cas_min_u128(p.split_new + j, ord64(comp), ord64(entry), guess, &tries);
+    const bool won = cas_min_u128(t.split + j, ord64(comp), ord64(entry), guess, &tries);
     if (p.prof) {
         atomicAdd(&p.ctrl->st[ST_CAS_ANGLE_CALLS], 1ull);
         atomicAdd(&p.ctrl->st[ST_CAS_ANGLE_TRIES], (unsigned long long)tries);
@@ -373,11 +395,14 @@ __device__ __forceinline__ void angle_event(const Params &p, Stage &sg, int32_t 
     }
 }
 
-__device__ __forceinline__ void fan_event(const Params &p, Stage &sg, int it, unsigned long long *nf_glob,
-                                          FanEv *fe_out, ulonglong2 guess, int32_t v, int32_t anchor,
-                                          double cand, double ax, double ay, double bx, double by) {
+__device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uint32_t row, Stage &sg,
+                                          unsigned long long *nf_glob, FanEv *fe_out, ulonglong2 guess,
+                                          int32_t v, int32_t anchor, double cand, double ax, double ay,
+                                          double bx, double by) {
     FanEv e;
     e.v = v;
+    e.row = row;
+    e.pad = 0u;
     e.anchor = anchor;
     e.cand = cand;
     e.ax = ax;
@@ -394,7 +419,7 @@ __device__ __forceinline__ void fan_event(const Params &p, Stage &sg, int it, un
     const unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
     const unsigned long long lo = fan_tiebreak(e);
     int tries = 0;
-    cas_min_u128(p.fanpick[p.live ? 0 : it % 3] + v, hi, lo, guess, &tries);
+    cas_min_u128(t.pick + v, hi, lo, guess, &tries);
     if (p.prof) {
         atomicAdd(&p.ctrl->st[ST_CAS_FAN_CALLS], 1ull);
         atomicAdd(&p.ctrl->st[ST_CAS_FAN_TRIES], (unsigned long long)tries);
@@ -530,8 +555,9 @@ __device__ __forceinline__ bool fan_span(const Params &p, int32_t v, int32_t anc
 // interval.  `fresh` filters against the shadow field of this iteration
 // (phase B, where the frozen copy is being committed) instead of gdist.
 template <typename Emit>
-__device__ __forceinline__ void fan_item(const Params &p, double cand, const FanSpan &f, int i,
-                                         int rep, bool fresh, Emit &&emit, LocalStats &ls) {
+__device__ __forceinline__ void fan_item(const Params &p, const RowTabs &t, uint32_t row, double cand,
+                                         const FanSpan &f, int i, int rep, bool fresh, Emit &&emit,
+                                         LocalStats &ls) {
     const FanRec &fr = p.fan[f.off + i];
     double wlo = __ldg(&fr.wlo), whi = __ldg(&fr.whi);
     double lo = f.flo - rep * f.theta, hi = f.fhi - rep * f.theta;
@@ -566,16 +592,17 @@ __device__ __forceinline__ void fan_item(const Params &p, double cand, const Fan
     const uint32_t cv1 = (uint32_t)qid | ((sad & 2u) ? SADDLE_BIT : 0u);
     double gp, gq;
     if (fresh) {
-        gp = __longlong_as_double((long long)__ldcg(p.dist_new + pid));
-        gq = __longlong_as_double((long long)__ldcg(p.dist_new + qid));
+        gp = __longlong_as_double((long long)__ldcg(t.dist + pid));
+        gq = __longlong_as_double((long long)__ldcg(t.dist + qid));
     } else {
-        gp = gdist(p, pid);
-        gq = gdist(p, qid);
+        gp = gdist(p, t, pid);
+        gq = gdist(p, t, qid);
     }
     Win c;
     int fate = make_child(__ldg(&fr.che), __ldg(&fr.cho), cv0, cv1, __ldg(&fr.capx), __ldg(&fr.lc), px, py,
                           qx, qy, s0, s1, 0.0, 0.0, cand,
                           gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, c);
+    c.row = row;
     if (fate == CH_STORED) {
         emit(c);
     } else {
@@ -588,12 +615,12 @@ __device__ __forceinline__ void fan_item(const Params &p, double cand, const Fan
 // incoming ray; `full` emits every wedge (source initialisation).  Serial
 // form (one thread); the solver loop spreads fan items over a warp.
 template <typename Emit>
-__device__ void emit_fan(const Params &p, int32_t v, double cand, int32_t anchor, double rel,
-                         bool full, Emit &&emit, LocalStats &ls) {
+__device__ void emit_fan(const Params &p, const RowTabs &t, uint32_t row, int32_t v, double cand,
+                         int32_t anchor, double rel, bool full, Emit &&emit, LocalStats &ls) {
     FanSpan f;
     if (!fan_span(p, v, anchor, rel, full, f)) return;
     for (int i = 0; i < f.m; ++i)
-        for (int rep = 0; rep < f.reps; ++rep) fan_item(p, cand, f, i, rep, false, emit, ls);
+        for (int rep = 0; rep < f.reps; ++rep) fan_item(p, t, row, cand, f, i, rep, false, emit, ls);
 }
 
 // ---------------------------------------------------------------------------
@@ -616,6 +643,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     const int32_t j = w.he, jo = w.jo;
     const double b0 = w.b0, b1 = w.b1, d0 = w.d0, d1 = w.d1, dps = w.d;
     const bool far = jo >= 0;
+    const RowTabs T = row_tabs(p, w.row, it);
     // level 1: the far face (or, on a boundary, the window's own face)
     // and the angle-split entry of j
     const int32_t fr = far ? jo : j;
@@ -633,14 +661,14 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     const int32_t cho_l = __ldg(&fp->opp[a1]), cho_r = __ldg(&fp->opp[a2]);
     const uint32_t apx_l = __ldg(&fp->apx[a1]), apx_r = __ldg(&fp->apx[a2]);
     ulonglong2 sp_raw = make_ulonglong2(0ull, 0ull);
-    const double2 sp = far ? gsplit(p, j, sp_raw) : make_double2(INFINITY, 0.0);
+    const double2 sp = far ? gsplit(p, T, j, sp_raw) : make_double2(INFINITY, 0.0);
     // level 2: distances at the three vertices
     const int32_t v0 = (int32_t)(v0f & VMASK), v1 = (int32_t)(v1f & VMASK);
     const int32_t vd = (int32_t)(vdf & VMASK);
-    const double g0 = gdist(p, v0), g1 = gdist(p, v1);
-    const double gdd = far ? gdist(p, vd) : INFINITY;
+    const double g0 = gdist(p, T, v0), g1 = gdist(p, T, v1);
+    const double gdd = far ? gdist(p, T, vd) : INFINITY;
     // saddle endpoints: the current fan pick, the guess for its CAS-min
-    const ulonglong2 *pick = p.fanpick[p.live ? 0 : it % 3];
+    const ulonglong2 *pick = T.pick;
     const ulonglong2 none = make_ulonglong2(~0ull, ~0ull);
     const ulonglong2 pk0 = (p.live && (v0f & SADDLE_BIT)) ? __ldcg(pick + v0) : none;
     const ulonglong2 pk1 = (p.live && (v1f & SADDLE_BIT)) ? __ldcg(pick + v1) : none;
@@ -717,6 +745,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     const int frr = make_child(3 * (fr / 3) + a2, cho_r, vdf, v1f, apx_r, lpv, dx, dy, ell, 0.0,
                                occ ? 0.0 : rA, rB,
                                ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, cr);
+    cl.row = cr.row = w.row;
     const bool ml = want_l && okL, mr = want_r && okR;  // children computed
     const bool sl = ml && fl == CH_STORED, sr = mr && frr == CH_STORED;
     // accounting as the reference counts it (geom.py:433-516)
@@ -738,19 +767,19 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     }
 
     // ---- events, issued together (order independent: min / CAS-min) ----
-    if (ev0) dist_event(p, sg, v0, cand0, ls);
-    if (ev1) dist_event(p, sg, v1, cand1, ls);
-    if (evd) dist_event(p, sg, vd, candd, ls);
-    if (claim) angle_event(p, sg, j, comp, entry_x, sp_raw, ls);
+    if (ev0) dist_event(p, T, sg, v0, cand0, ls);
+    if (ev1) dist_event(p, T, sg, v1, cand1, ls);
+    if (evd) dist_event(p, T, sg, vd, candd, ls);
+    if (claim) angle_event(p, T, sg, j, comp, entry_x, sp_raw, ls);
     // saddle fans (Fig. 3c): the reverse direction of the incoming ray
     // relative to an anchor half-edge out of the vertex (geom.py:353-484)
-    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, sg, it, nf_glob, fe_out, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
+    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, sg, nf_glob, fe_out, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
     if (ev1 && (v1f & SADDLE_BIT)) {
         if (far) {
             // anchor jo = v1 -> v0: its wedge follows next(j)'s, so this is
             // the reference's anchor next(j) with the corner at v1 folded
             // into the anchor angle
-            fan_event(p, sg, it, nf_glob, fe_out, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
+            fan_event(p, T, w.row, sg, nf_glob, fe_out, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
         } else {
             // boundary window: anchor next(j), the source-side apex
             // direction from v1 (geom.py:372-377)
@@ -761,12 +790,12 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
             const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
             const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
             const double ay2 = lps * lps - axs * axs;
-            fan_event(p, sg, it, nf_glob, fe_out, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
+            fan_event(p, T, w.row, sg, nf_glob, fe_out, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
                       ay2 > 0.0 ? sqrt(ay2) : 0.0);
         }
     }
     if (evd && (vdf & SADDLE_BIT))
-        fan_event(p, sg, it, nf_glob, fe_out, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
+        fan_event(p, T, w.row, sg, nf_glob, fe_out, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
     return nc;
 }
 
@@ -994,13 +1023,13 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                         if (lane == 0) ls.add(ST_FANS);
                         const int items = f.m * f.reps;
                         if (lane < items) {
-                            fan_item(p, e.cand, f, lane % f.m, lane / f.m, false,
+                            fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, lane % f.m, lane / f.m, false,
                                      [&](const Win &x) { c = x; n = 1; }, ls);
                         }
                         // wedges beyond the warp width (valence > 32): rare,
                         // appended with a warp-aggregated global slot
                         for (int q = lane + 32; q < items; q += 32)
-                            fan_item(p, e.cand, f, q % f.m, q / f.m, false,
+                            fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, q % f.m, q / f.m, false,
                                      [&](const Win &x) { put_pool(x, warp_alloc(&cur.nC, true)); }, ls);
                     }
                     if (p.prof) {
@@ -1310,8 +1339,9 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                 const int sl = lane % FAN_LANES;
                 if (fi < nF) {
                     const FanEv e = fev[fi];
-                    const unsigned long long dv = __ldcg(p.dist_new + e.v);
-                    const ulonglong2 pk = __ldcg(p.fanpick[0] + e.v);
+                    const RowTabs T = row_tabs(p, e.row, it);
+                    const unsigned long long dv = __ldcg(T.dist + e.v);
+                    const ulonglong2 pk = __ldcg(T.pick + e.v);
                     const double rel = fan_rel(e);
                     const unsigned long long hi = (unsigned long long)__double_as_longlong(e.cand);
                     const unsigned long long lo = fan_tiebreak(e);
@@ -1325,10 +1355,10 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
                         if (sl == 0) ls.add(ST_FANS);
                         const int items = f.m * f.reps;
                         if (sl < items)
-                            fan_item(p, e.cand, f, sl % f.m, sl / f.m, false,
+                            fan_item(p, T, e.row, e.cand, f, sl % f.m, sl / f.m, false,
                                      [&](const Win &x) { o0 = x; no = 1; }, ls);
                         for (int q = sl + FAN_LANES; q < items; q += FAN_LANES)
-                            fan_item(p, e.cand, f, q % f.m, q / f.m, false, put_direct, lsd);
+                            fan_item(p, T, e.row, e.cand, f, q % f.m, q / f.m, false, put_direct, lsd);
                     }
                 }
                 if (p.prof) {
@@ -1458,28 +1488,34 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
 __global__ void k_init_state(Params p, const int64_t *src, int nsrc) {
     const long long n = (long long)gridDim.x * blockDim.x;
     const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    for (long long v = t0; v < p.nv; v += n) {
-        p.dist_cur[v] = INFINITY;
+    const long long nvr = (long long)p.nv * p.rows, nher = (long long)p.nhe * p.rows;
+    for (long long v = t0; v < nvr; v += n) {
         p.dist_new[v] = (unsigned long long)__double_as_longlong(INFINITY);
         p.fanpick[0][v] = make_ulonglong2(~0ull, ~0ull);
-        p.fanpick[1][v] = make_ulonglong2(~0ull, ~0ull);
-        p.fanpick[2][v] = make_ulonglong2(~0ull, ~0ull);
     }
-    for (long long j = t0; j < p.nhe; j += n) {
-        p.split_cur[j] = make_double2(INFINITY, 0.0);
-        p.split_new[j] = make_ulonglong2(ord64(INFINITY), ord64(0.0));
+    if (!p.live) {
+        for (long long v = t0; v < p.nv; v += n) {
+            p.dist_cur[v] = INFINITY;
+            p.fanpick[1][v] = make_ulonglong2(~0ull, ~0ull);
+            p.fanpick[2][v] = make_ulonglong2(~0ull, ~0ull);
+        }
+        for (long long j = t0; j < p.nhe; j += n) p.split_cur[j] = make_double2(INFINITY, 0.0);
     }
+    for (long long j = t0; j < nher; j += n) p.split_new[j] = make_ulonglong2(ord64(INFINITY), ord64(0.0));
     for (long long b = t0; b < 2 * (NBINS + 1); b += n) (b <= NBINS ? p.hist[0][b] : p.hist[1][b - NBINS - 1]) = 0u;
     if (t0 == 0)
         for (int q = 0; q < NSLOT; ++q) p.ctrl->slot[q].pmin = ~0ull;
 }
 
+// one field (rows == 1: the union of the sources, reference run_pch) or
+// one field per source (batched rows: source i seeds row i)
 __global__ void k_set_sources(Params p, const int64_t *src, int nsrc) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nsrc) {
-        int64_t s = src[i];
-        p.dist_cur[s] = 0.0;
-        p.dist_new[s] = 0ull;
+        const int64_t s = src[i];
+        const size_t r = p.rows > 1 ? (size_t)i : 0;
+        if (!p.live) p.dist_cur[s] = 0.0;
+        p.dist_new[r * p.nv + s] = 0ull;
     }
 }
 
@@ -1500,7 +1536,10 @@ __global__ void k_source_windows(Params p, const int64_t *src, int nsrc) {
     if (i < nsrc) {
         int32_t s = (int32_t)src[i];
         if ((__double_as_longlong(__ldg(&p.fanhdr[s].meta_bits)) >> 32) & 0x7fffffffll)
-            emit_fan(p, s, 0.0, 0, 0.0, true, emit, ls);
+        {
+            const uint32_t r = p.rows > 1 ? (uint32_t)i : 0u;
+            emit_fan(p, row_tabs(p, r, 0), r, s, 0.0, 0, 0.0, true, emit, ls);
+        }
     }
     flush_stats(ctrl, s_st);
 }
@@ -1542,6 +1581,7 @@ struct pch_mesh {
     size_t mesh_bytes = 0;
     // workspace
     long long cap = 0;
+    int rows_alloc = 0;
     std::vector<void *> ws;
     Params prm{};
     int64_t *d_src = nullptr;
@@ -1580,7 +1620,7 @@ static int ws_alloc(pch_mesh *m, T **out, size_t count) {
 static int alloc_soa(pch_mesh *m, WinSoA &W, long long cap) {
     int rc;
     if ((rc = ws_alloc(m, &W.hv, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.vd, cap))) return rc;
+    if ((rc = ws_alloc(m, &W.vr, cap))) return rc;
     if ((rc = ws_alloc(m, &W.b0, cap))) return rc;
     if ((rc = ws_alloc(m, &W.b1, cap))) return rc;
     if ((rc = ws_alloc(m, &W.d0, cap))) return rc;
@@ -1590,8 +1630,10 @@ static int alloc_soa(pch_mesh *m, WinSoA &W, long long cap) {
     return PCH_OK;
 }
 
-static int ensure_ws(pch_mesh *m, long long cap) {
-    if (m->cap >= cap) return PCH_OK;
+static int ensure_ws(pch_mesh *m, long long cap, int rows) {
+    if (m->cap >= cap && m->rows_alloc >= rows) return PCH_OK;
+    cap = std::max(cap, m->cap);
+    rows = std::max(rows, m->rows_alloc);
     free_ws(m);
     Params &p = m->prm;
     int rc;
@@ -1603,10 +1645,10 @@ static int ensure_ws(pch_mesh *m, long long cap) {
     p.nv = m->nv;
     p.nhe = m->nhe;
     if ((rc = ws_alloc(m, &p.dist_cur, m->nv))) return rc;
-    if ((rc = ws_alloc(m, &p.dist_new, m->nv))) return rc;
+    if ((rc = ws_alloc(m, &p.dist_new, (size_t)m->nv * rows))) return rc;
     if ((rc = ws_alloc(m, &p.split_cur, m->nhe))) return rc;
-    if ((rc = ws_alloc(m, &p.split_new, m->nhe))) return rc;
-    if ((rc = ws_alloc(m, &p.fanpick[0], m->nv))) return rc;
+    if ((rc = ws_alloc(m, &p.split_new, (size_t)m->nhe * rows))) return rc;
+    if ((rc = ws_alloc(m, &p.fanpick[0], (size_t)m->nv * rows))) return rc;
     if ((rc = ws_alloc(m, &p.fanpick[1], m->nv))) return rc;
     if ((rc = ws_alloc(m, &p.fanpick[2], m->nv))) return rc;
     // one entry per improving event of an iteration (<= 3 per propagated
@@ -1628,21 +1670,29 @@ static int ensure_ws(pch_mesh *m, long long cap) {
     if ((rc = ws_alloc(m, &p.ctrl, 1))) return rc;
     p.cap = cap;
     m->cap = cap;
+    m->rows_alloc = rows;
     return PCH_OK;
 }
 
+// rows == 1: one field from the union of the sources (reference run_pch);
+// rows == nsrc > 1: one field per source, solved together (batched rows,
+// live solver only)
 static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *cfg,
-                 cudaStream_t st, pch_stats *stats) {
+                 cudaStream_t st, pch_stats *stats, int rows = 1) {
     if (cfg->k < 1) return fail(PCH_ERR_CONFIG, "k must be >= 1");
     if (!(cfg->epsilon_window > 0.0)) return fail(PCH_ERR_CONFIG, "epsilon_window must be > 0");
     if (cfg->fan_mode != 0 && cfg->fan_mode != 1) return fail(PCH_ERR_CONFIG, "fan_mode must be clip or full_edges");
     if (cfg->chain < 0) return fail(PCH_ERR_CONFIG, "chain must be >= 0");
-    long long cap = cfg->pool_capacity > 0 ? cfg->pool_capacity
-                                           : std::max<long long>(1 << 20, 2ll * m->nhe);
+    if (rows > 1 && (cfg->flags & PCH_FLAG_DETERMINISTIC))
+        return fail(PCH_ERR_CONFIG, "batched rows need the live solver");
+    // the pool holds every row's wavefront: scale the first guess with rows
+    long long cap = cfg->pool_capacity > 0
+                        ? cfg->pool_capacity
+                        : std::max<long long>(1 << 20, 2ll * m->nhe) * std::max(1, rows / 4);
     if (m->cap > cap) cap = m->cap;
     int regrows = 0;
     for (;;) {
-        int rc = ensure_ws(m, cap);
+        int rc = ensure_ws(m, cap, rows);
         if (rc) return rc;
         Params p = m->prm;
         p.K = cfg->k;
@@ -1653,6 +1703,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.fan_full = cfg->fan_mode == 1;
         p.recheck = (cfg->flags & PCH_FLAG_NO_RECHECK) ? 0 : 1;
         p.live = (cfg->flags & PCH_FLAG_DETERMINISTIC) ? 0 : 1;
+        p.rows = rows;
         // step controller bounds (mean edge lengths): the floor keeps wide
         // wavefronts (tori, large spheres: far more than k windows per face
         // layer) from splitting one layer over many iterations; measured
@@ -1995,9 +2046,14 @@ int pch_run_rows(pch_mesh *m, const int64_t *sources, int64_t n_sources, const p
     if (rc) return rc;
     CK(cudaSetDevice(m->device));
     if ((rc = stage_sources(m, sources, n_sources))) return rc;
-    for (int64_t r = 0; r < n_sources; ++r) {
-        if ((rc = solve(m, m->d_src + r, 1, cfg, m->stream, stats))) return rc;
-        CK(cudaMemcpyAsync(out_rows + r * (int64_t)m->nv, field_ptr(m), sizeof(double) * m->nv,
+    // batches of R fields solved together (one field per source); the
+    // deterministic solver runs them one at a time
+    int R = (cfg->flags & PCH_FLAG_DETERMINISTIC) ? 1 : DEFAULT_ROWS;
+    if (const char *rr = getenv("PCH_ROWS")) R = std::max(1, atoi(rr));  // development
+    for (int64_t r0 = 0; r0 < n_sources; r0 += R) {
+        const int n = (int)std::min<int64_t>(R, n_sources - r0);
+        if ((rc = solve(m, m->d_src + r0, n, cfg, m->stream, stats, n))) return rc;
+        CK(cudaMemcpyAsync(out_rows + r0 * (int64_t)m->nv, field_ptr(m), sizeof(double) * m->nv * n,
                            cudaMemcpyDeviceToHost, m->stream));
     }
     CK(cudaStreamSynchronize(m->stream));

@@ -202,6 +202,40 @@ def run_reference(args):
     return 0
 
 
+def _rows_leg(args, ws, rank, local, dev):
+    """BASELINE configs[4]: distance-matrix rows on the 500k-face torus,
+    sources sharded over the ranks (each GPU a mesh replica, batched rows
+    through pch_run_rows), rows all-gathered over NCCL at the end; wall
+    time of the whole job (max over ranks), inputs and outputs on the host."""
+    import torch
+    from paper_1305_1293_b200 import EngineConfig, run_pch_rows
+    from paper_1305_1293_b200.shard import gather_rows, shard_sources
+    mesh, _ = _workload("torus500k")
+    total = args.rows_per_rank * ws
+    srcs = np.random.default_rng(4096).choice(mesh.n_vertices, total, replace=False)
+    mine = srcs[shard_sources(srcs, rank, ws)]
+    cfg = EngineConfig(device=local)
+    run_pch_rows(mesh, mine[:8], cfg)  # warm-up: upload, workspace
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    rows, st = run_pch_rows(mesh, mine, cfg)
+    if ws > 1:
+        gather_rows(rows, total, rank, ws, device=dev)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t
+    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    dt = float(tt.item())
+    return {"workload": "torus500k", "faces": int(mesh.n_faces), "sources": int(total),
+            "sources_per_sec": round(total / dt, 2), "seconds": round(dt, 3), "n_gpus": ws,
+            "scaling": "weak", "batch_rows": 32,
+            "windows_per_source": int(st.total_windows_created // max(len(mine), 1)),
+            "timing": "wall clock, host sources in / host rows out, NCCL all-gather included"}
+
+
 def run_b200(args):
     import torch
     ws, rank, local = _dist_env()
@@ -274,6 +308,8 @@ def run_b200(args):
     assert np.array_equal(np.isfinite(host), fin), "host and device entry points disagree"
     assert np.all(np.abs(host[fin] - field[fin]) <= 1e-9 * np.maximum(np.abs(field[fin]), 1e-12))
 
+    rows_info = None if args.rows_per_rank <= 0 else _rows_leg(args, ws, rank, local, dev)
+
     tot = torch.tensor([dev_ms, e2e_ms, kern_ms], dtype=torch.float64, device=dev)
     if ws > 1:
         torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
@@ -313,6 +349,8 @@ def run_b200(args):
                         "windows_per_sec": round(propagated / (kern_ms * 1e-3), 1)},
             "clocks": clk.summary(),
         }
+        if rows_info is not None:
+            line["rows"] = rows_info
         if ws == 1 and not args.no_cpu_baseline:
             ref, ich, cb = _cpu_baseline(mesh, src)
             fin = np.isfinite(ref)
@@ -338,6 +376,8 @@ def main(argv=None):
     ap.add_argument("--k", type=int, default=16384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
+    ap.add_argument("--rows-per-rank", type=int, default=64,
+                    help="configs[4] distance-matrix rows per GPU (0 = skip)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

@@ -352,6 +352,7 @@ constexpr int NWARP = TPB / 32;
 constexpr double DELTA_FLOOR = 0.15;  // controller step floor, mean edge lengths
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
+constexpr int WIDE_ROWS = 8;          // from this many rows on, the 2-CTA/SM solver
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
@@ -1166,7 +1167,12 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
 //     only weakens pruning).  Fields agree across runs to rounding; the
 //     bitwise-deterministic two-barrier kernel above is PCH_FLAG_DETERMINISTIC.
 
-__global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_live(Params p) {
+// MINB = resident CTAs per SM the register budget targets: 1 for single
+// fields (latency bound: the propagation chain, 216 registers, no spills),
+// 2 for batched rows (throughput bound: twice the warps per SM hide the
+// chain's latency, at the price of a few register spills)
+template <int MINB>
+__global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
     Ctrl *ctrl = p.ctrl;
     unsigned int gen = 0;
     __shared__ unsigned long long s_st[N_ST];
@@ -1589,7 +1595,7 @@ struct pch_mesh {
     double *d_out = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
-    int grid = 0, grid_live = 0;
+    int grid = 0, grid_live = 0, grid_live2 = 0;
     unsigned long long *trace = nullptr;  // PCH_TRACE development timeline
     long long trace_cap = 0;
 };
@@ -1741,7 +1747,12 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         CK(cudaEventRecord(m->ev1, st));
         void *args[] = {&p};
         if (p.live)
-            CK(cudaLaunchCooperativeKernel((const void *)pch_live, dim3(m->grid_live), dim3(TPB), args, 0, st));
+        {
+            const bool wide = rows >= WIDE_ROWS && m->grid_live2 > 0;
+            const void *kern = wide ? (const void *)pch_live<2> : (const void *)pch_live<1>;
+            CK(cudaLaunchCooperativeKernel(kern, dim3(wide ? m->grid_live2 : m->grid_live), dim3(TPB), args,
+                                           0, st));
+        }
         else
             CK(cudaLaunchCooperativeKernel((const void *)pch_persistent, dim3(m->grid), dim3(TPB), args, 0, st));
         CK(cudaEventRecord(m->ev2, st));
@@ -1964,11 +1975,14 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
     int nsm = 0, per_sm = 0, per_sm_live = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_persistent, TPB, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live, TPB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live<1>, TPB, 0);
+    int per_sm_live2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live2, pch_live<2>, TPB, 0);
     if (per_sm < 1 || per_sm_live < 1) return cleanup(PCH_ERR_CUDA, "persistent kernel cannot be resident");
     // persistent grids: every SM, as many co-resident CTAs as fit (<= 4)
     m->grid = nsm * std::min(per_sm, 4);
     m->grid_live = nsm * std::min(per_sm_live, 4);
+    m->grid_live2 = per_sm_live2 >= 2 ? nsm * std::min(per_sm_live2, 4) : 0;
     *out = m;
     return PCH_OK;
 }

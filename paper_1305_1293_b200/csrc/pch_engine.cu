@@ -1,33 +1,29 @@
 // pch_engine.cu -- B200-native Parallel Chen-Han exact geodesic solver.
 //
-// One persistent cooperative kernel runs the whole PCH loop (paper
+// A persistent cooperative kernel runs the whole PCH loop (paper
 // Algorithm 1; reference pkg/src/pargeo/engine.py:433 run_pch) on the
-// device.  Each iteration is two phases separated by grid barriers, so
-// the per-level CPU/GPU synchronisation the paper identifies as the CH
-// bottleneck never happens:
+// device, so the per-level CPU/GPU synchronisation the paper identifies as
+// the CH bottleneck never happens.  Two solvers share the window geometry
+// (pch_device.cuh, reference geom.py) and the event primitives:
 //
-//   phase A  (propagate)  every thread takes windows of the selected batch
-//            S_i and runs Algorithm 2 (geom.py:312) against the *frozen*
-//            distance field and angle-split table of the previous
-//            iteration; children are appended to the pool (warp-aggregated
-//            slot allocation), their keys histogrammed; distance events
-//            are 64-bit atomicMin on the fp64 bit patterns of a shadow
-//            field, angle events a 128-bit CAS-min of (comp, entry_x) on a
-//            shadow split table; saddle fans of the previous iteration's
-//            winners are emitted here too.
-//   phase B  (organise)   the k-selection threshold t_{i+1} is read off the
-//            key histogram (distance-threshold pick, every CTA computes the
-//            same value); touched vertices / angles are committed from the
-//            shadow tables; the pool P_i + children C_i is partitioned into
-//            the next batch S_{i+1} (key <= t) and the next pool P_{i+1}
-//            (stream compaction, gap free -- paper Algorithm 3), whose keys
-//            are histogrammed for the following threshold.
+//   pch_live (default)   one phase + one grid barrier per iteration: the
+//            next threshold is fixed up front by a step controller, every
+//            produced window is routed to the next batch or the pool as it
+//            is produced (CTA-wide scan, one reservation per CTA), the
+//            filters read the tables the events update atomically, and a
+//            child inside the next threshold is propagated at once by the
+//            same thread (chaining).  Also solves R fields at once
+//            (batched rows, pch_run_rows).
+//   pch_persistent (PCH_FLAG_DETERMINISTIC)   two phases per iteration:
+//            propagation against tables frozen at the start of the
+//            iteration, then commit + histogram k-selection + partition
+//            (paper Algorithm 3) -- bitwise reproducible.
 //
-// Deferred event application replaces the paper's sort-then-first-wins
-// pass (Algorithm 4; engine.py:341/:359): atomicMin is order independent,
-// so results do not depend on scheduling.  Saddle fans are deferred one
-// iteration and emitted once per vertex by the smallest candidate
-// (window-count control).
+// In both, events replace the paper's sort-then-first-wins pass
+// (Algorithm 4; engine.py:341/:359) by order-independent atomics: 64-bit
+// atomicMin on the fp64 bit patterns of the distance field, 128-bit
+// CAS-min of (comp, entry_x) on the angle-split table, and a per-vertex
+// CAS-min pick so each improved saddle fans out once.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 

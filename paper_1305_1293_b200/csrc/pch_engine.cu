@@ -115,6 +115,8 @@ struct Params {
     int prof;                  // PCH_PROFILE: accumulate per-section clocks
     int chain;                 // max propagations a thread chains per iteration
     int rows;                  // distance fields solved together (batched rows)
+    unsigned int *ccnt;        // live solver: per-CTA output counts [2 parity][S, P, fans][MAX_CTAS]
+    int live_grid;             // CTAs of the live solver's launch (chunk count)
     unsigned long long *trace; // optional per-iteration timeline (TR_* records)
     long long trace_cap;       // iterations the trace buffer holds
 };
@@ -349,6 +351,7 @@ constexpr double DELTA_FLOOR = 0.15;  // controller step floor, mean edge length
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
 constexpr int WIDE_ROWS = 8;          // from this many rows on, the 2-CTA/SM solver
+constexpr int MAX_CTAS = 1024;        // chunk-count tables of the live solver
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
@@ -392,10 +395,10 @@ __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, S
     }
 }
 
-__device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uint32_t row, Stage &sg,
-                                          unsigned long long *nf_glob, FanEv *fe_out, ulonglong2 guess,
-                                          int32_t v, int32_t anchor, double cand, double ax, double ay,
-                                          double bx, double by) {
+template <typename FanSink>
+__device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uint32_t row, FanSink &&sink,
+                                          ulonglong2 guess, int32_t v, int32_t anchor, double cand,
+                                          double ax, double ay, double bx, double by) {
     FanEv e;
     e.v = v;
     e.row = row;
@@ -421,16 +424,28 @@ __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uin
         atomicAdd(&p.ctrl->st[ST_CAS_FAN_CALLS], 1ull);
         atomicAdd(&p.ctrl->st[ST_CAS_FAN_TRIES], (unsigned long long)tries);
     }
-    const unsigned int k = atomicAdd(&sg.nfe, 1u);
-    if (k < (unsigned int)FE_CAP) {
-        sg.fe[k] = e;
-    } else {
-        atomicSub(&sg.nfe, 1u);
-        const unsigned long long at = atomicAdd(nf_glob, 1ull);
-        if ((long long)at < p.fancap) fe_out[at] = e;
-        else atomicExch(&p.ctrl->error, ERR_OVERFLOW);
-    }
+    sink(e);
 }
+
+// fan candidates of the deterministic solver: staged in shared memory and
+// flushed by the CTA per trip (trip_flush); overflow appends directly
+struct StageFanSink {
+    const Params &p;
+    Stage &sg;
+    unsigned long long *nf_glob;
+    FanEv *fe_out;
+    __device__ __forceinline__ void operator()(const FanEv &e) const {
+        const unsigned int k = atomicAdd(&sg.nfe, 1u);
+        if (k < (unsigned int)FE_CAP) {
+            sg.fe[k] = e;
+        } else {
+            atomicSub(&sg.nfe, 1u);
+            const unsigned long long at = atomicAdd(nf_glob, 1ull);
+            if ((long long)at < p.fancap) fe_out[at] = e;
+            else atomicExch(&p.ctrl->error, ERR_OVERFLOW);
+        }
+    }
+};
 
 // End of one trip of the selected batch (uniform over the CTA): reserve
 // `n` (<= 2) pool slots per thread for the children with one global
@@ -624,9 +639,9 @@ __device__ void emit_fan(const Params &p, const RowTabs &t, uint32_t row, int32_
 // Algorithm 2 (geom.py:312) for one window against the frozen tables.
 // Up to two children are returned in `c`; events go to the shadow tables.
 
-__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, unsigned long long *nf_glob,
-                                         FanEv *fe_out, const Win &w, Win &out0, Win &out1,
-                                         LocalStats &ls) {
+template <typename FanSink>
+__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, FanSink &&fsink,
+                                         const Win &w, Win &out0, Win &out1, LocalStats &ls) {
     // Latency layout: the per-iteration critical path is one propagation
     // (of the slowest lane of the slowest warp), so
     //  * every memory access is issued as soon as its address is known
@@ -770,13 +785,13 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
     if (claim) angle_event(p, T, sg, j, comp, entry_x, sp_raw, ls);
     // saddle fans (Fig. 3c): the reverse direction of the incoming ray
     // relative to an anchor half-edge out of the vertex (geom.py:353-484)
-    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, sg, nf_glob, fe_out, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
+    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, fsink, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
     if (ev1 && (v1f & SADDLE_BIT)) {
         if (far) {
             // anchor jo = v1 -> v0: its wedge follows next(j)'s, so this is
             // the reference's anchor next(j) with the corner at v1 folded
             // into the anchor angle
-            fan_event(p, T, w.row, sg, nf_glob, fe_out, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
+            fan_event(p, T, w.row, fsink, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
         } else {
             // boundary window: anchor next(j), the source-side apex
             // direction from v1 (geom.py:372-377)
@@ -787,12 +802,12 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, uns
             const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
             const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
             const double ay2 = lps * lps - axs * axs;
-            fan_event(p, T, w.row, sg, nf_glob, fe_out, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
+            fan_event(p, T, w.row, fsink, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
                       ay2 > 0.0 ? sqrt(ay2) : 0.0);
         }
     }
     if (evd && (vdf & SADDLE_BIT))
-        fan_event(p, T, w.row, sg, nf_glob, fe_out, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
+        fan_event(p, T, w.row, fsink, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
     return nc;
 }
 
@@ -977,7 +992,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 if (i < nS) {
                     long long c0 = p.prof ? clock64() : 0;
                     Win win = load_win(p.S, i);
-                    nc = propagate(p, sg, it, &cur.nF, p.fanev[it % 3], win, ca, cb, ls);
+                    nc = propagate(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, win, ca, cb, ls);
                     if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
                     if (nc > maxchild) maxchild = nc;
                 }
@@ -1167,55 +1182,126 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
 // fields (latency bound: the propagation chain, 216 registers, no spills),
 // 2 for batched rows (throughput bound: twice the warps per SM hide the
 // chain's latency, at the price of a few register spills)
+// Item index -> slot of a chunked buffer: chunk c holds items
+// [pre[c], pre[c+1]) at slots c * ch + (i - pre[c]) (binary search over the
+// CTA prefix table in shared memory).
+__device__ __forceinline__ unsigned long long chunk_slot(const unsigned int *pre, int G, unsigned int i,
+                                                         unsigned long long ch) {
+    int lo = 0, hi = G;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] <= i) lo = mid;
+        else hi = mid;
+    }
+    return (unsigned long long)lo * ch + (i - pre[lo]);
+}
+
+// warp-level reservation in the CTA's own chunk: every lane brings `n`
+// items, gets its first slot index (relative to the chunk); one shared
+// atomic per warp (converged warp)
+__device__ __forceinline__ unsigned int warp_chunk_alloc(unsigned int *s_cnt, unsigned int n) {
+    const int lane = threadIdx.x & 31;
+    unsigned int x = n;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    const unsigned int total = __shfl_sync(0xffffffffu, x, 31);
+    unsigned int base = 0;
+    if (lane == 31 && total) base = atomicAdd(s_cnt, total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    return base + x - n;
+}
+
+// MINB = resident CTAs per SM the register budget targets: 1 for single
+// fields (latency bound: the propagation chain, no spills), 2 for batched
+// rows (throughput bound: twice the warps per SM hide the chain's latency,
+// at the price of some register spills)
 template <int MINB>
 __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
+    // Outputs are chunked per CTA: CTA b writes the windows it routes to
+    // slots [b*ch, (b+1)*ch) of the next batch / pool and its fan
+    // candidates to [b*chF, (b+1)*chF), allocating with one shared atomic
+    // per warp -- no CTA-wide scan or global reservation on the iteration's
+    // critical path.  Each CTA publishes its three counts at the end of the
+    // iteration; after the barrier every CTA rebuilds the prefix tables.
     Ctrl *ctrl = p.ctrl;
     unsigned int gen = 0;
+    const int G = gridDim.x;
+    const int b = blockIdx.x;
     __shared__ unsigned long long s_st[N_ST];
-    __shared__ Stage sg;
-    __shared__ unsigned long long s_res[3];  // S / P / fan-list reservations of a trip
-    __shared__ unsigned long long s_pmin, s_smax, s_tw, s_tl, s_tf;
+    __shared__ Stage sg;                        // unused staging (shared helpers)
+    __shared__ unsigned int s_pre[3][MAX_CTAS + 1];  // prefix tables: S, P, fans(prev)
+    __shared__ unsigned int s_n[3];             // this CTA's outputs: S, P, fans
+    __shared__ unsigned long long s_pmin, s_smax;
+    __shared__ unsigned long long s_c[3];       // err, pmin, smax of the finished iteration
     stats_init(s_st);
     if (threadIdx.x == 0) {
         sg.ntv = sg.nte = sg.nfe = 0u;
         s_pmin = ~0ull;
         s_smax = 0ull;
-        s_tw = s_tl = s_tf = 0ull;
+        s_n[0] = s_n[1] = s_n[2] = 0u;
     }
-    __syncthreads();
-    LocalStats ls{s_st, false};   // packed per-thread counters, folded per trip
+    LocalStats ls{s_st, false};   // packed per-thread counters, folded every FOLD_TRIPS
     LocalStats lsd{s_st, true};   // rare paths: straight to shared memory
     int maxchild = 0;
-    int trips_since_fold = 0;
-    const unsigned long long gthreads = (unsigned long long)gridDim.x * TPB;
+    int iters_since_fold = 0;
+    const unsigned long long ch = (unsigned long long)p.cap / G;
+    const unsigned long long chF = (unsigned long long)p.fancap / G;
+    const unsigned long long gthreads = (unsigned long long)G * TPB;
     const unsigned long long nwarps = gthreads >> 5;
-    const unsigned long long gwid = (unsigned long long)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+    const unsigned long long gwid = (unsigned long long)(threadIdx.x >> 5) * G + b;
     const int lane = threadIdx.x & 31;
     const unsigned long long t_start = globaltimer();
     double t = 0.0;           // threshold S_i was selected with
     double delta = p.delta0;  // controller step
-    // the iteration's counters, read once per CTA by thread 0 (at the
-    // barrier) and broadcast through shared memory
-    __shared__ unsigned long long s_c[6];  // err, nS, nP, nF(prev), pmin, smax
+    // prefix tables of the iteration's inputs from the per-CTA counts
+    auto build_prefix = [&](int par_in, int par_fan) {
+        if (threadIdx.x < 96) {
+            const int q = threadIdx.x >> 5;  // 0: S, 1: P, 2: fans of the previous iteration
+            const unsigned int *cnt = p.ccnt + (size_t)((q < 2 ? par_in : par_fan) * 3 + q) * MAX_CTAS;
+            if (lane == 0) s_pre[q][0] = 0u;
+            // all loads first (one round trip), then the carried scans
+            constexpr int PER = 8;  // G <= 256 in one pass
+            for (int base = 0; base < G; base += 32 * PER) {
+                unsigned int v[PER];
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const int c = base + k * 32 + lane;
+                    v[k] = c < G ? __ldcg(cnt + c) : 0u;
+                }
+                unsigned int carry = base ? s_pre[q][base] : 0u;
+#pragma unroll
+                for (int k = 0; k < PER; ++k) {
+                    const int c = base + k * 32 + lane;
+                    unsigned int x = v[k];
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (c < G) s_pre[q][c + 1] = carry + x;
+                    carry += __shfl_sync(0xffffffffu, x, 31);
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    };
+    build_prefix(0, 1);  // S_0: the source windows (chunk-published by k_source_windows)
     if (threadIdx.x == 0) {
         s_c[0] = 0ull;
-        s_c[1] = *(volatile unsigned long long *)&ctrl->slot[0].nS;
-        s_c[2] = *(volatile unsigned long long *)&ctrl->slot[0].nP;
-        s_c[3] = 0ull;
-        s_c[4] = *(volatile unsigned long long *)&ctrl->slot[0].pmin;
-        s_c[5] = *(volatile unsigned long long *)&ctrl->slot[0].smax;
+        s_c[1] = *(volatile unsigned long long *)&ctrl->slot[0].pmin;
+        s_c[2] = *(volatile unsigned long long *)&ctrl->slot[0].smax;
     }
     __syncthreads();
     int it = 0;
     for (;;) {
-        Slot &cur = ctrl->slot[it % NSLOT];
+        const int par = it & 1;                     // parity of the iteration's inputs
+        const unsigned int nS = s_pre[0][G], nP = s_pre[1][G], nF = it > 0 ? s_pre[2][G] : 0u;
+        const unsigned long long pminb = s_c[1], smaxb = s_c[2];
         Slot &nxt = ctrl->slot[(it + 1) % NSLOT];
-        const unsigned long long nS = s_c[1];
-        const unsigned long long nP = s_c[2];
-        const unsigned long long nFr = s_c[3];
-        const unsigned long long pminb = s_c[4];
-        const unsigned long long smaxb = s_c[5];
-        const unsigned long long nF = nFr < (unsigned long long)p.fancap ? nFr : p.fancap;
         // step controller: |S_i| / k steers the distance step
         if (it > 0) {
             double f = (double)p.K / (double)(nS > 0 ? nS : 1);
@@ -1231,18 +1317,17 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
         if (nS > 0 && it > 0 && smax < t) t = smax;
         if (nS == 0 && pmin > t && pmin < INFINITY) t = pmin;
         const double tn = t + delta;  // threshold of S_{i+1}
-        const WinSoA Sc = (it & 1) ? p.S2 : p.S, Sn = (it & 1) ? p.S : p.S2;
-        const WinSoA Pc = (it & 1) ? p.Y : p.X, Pn = (it & 1) ? p.X : p.Y;
-        const FanEv *fev = p.fanev[(it + 1) & 1];  // fan candidates of iteration i-1
+        const WinSoA Sc = par ? p.S2 : p.S, Sn = par ? p.S : p.S2;
+        const WinSoA Pc = par ? p.Y : p.X, Pn = par ? p.X : p.Y;
+        const FanEv *fev = p.fanev[par ^ 1];        // fan candidates of iteration i-1
+        FanEv *fout = p.fanev[par] + (size_t)b * chF;  // this CTA's chunk for iteration i
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             // the slot of iteration i+2 is idle now: clear it
             Slot &clr = ctrl->slot[(it + 2) % NSLOT];
-            clr.nS = clr.nP = clr.nC = clr.nTV = clr.nTE = clr.nF = 0ull;
             clr.pmin = ~0ull;
             clr.smax = 0ull;
-            ls.max(ST_PEAK, nS + nP);
+            ls.max(ST_PEAK, (unsigned long long)nS + nP);
         }
-        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_START_MAX);
         if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *tr = p.trace + (size_t)it * TR_N;
             tr[TR_T0] = globaltimer();
@@ -1251,52 +1336,41 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
             tr[TR_NF] = nF;
             tr[TR_TSEL_BITS] = (unsigned long long)__double_as_longlong(tn);
         }
-        // route a window to S_{i+1} / P_{i+1} once its slot is known
-        auto put = [&](const WinSoA &W, unsigned long long at, const Win &c) {
-            if ((long long)at < p.cap) store_win(W, at, c);
+        // fan candidates of this iteration go straight to the CTA's chunk
+        auto fsink = [&](const FanEv &e) {
+            const unsigned int k = atomicAdd(&s_n[2], 1u);
+            if (k < chF) fout[k] = e;
             else atomicExch(&ctrl->error, ERR_OVERFLOW);
-            ls.add(ST_STORED);
         };
-        // rare path: a fan with more wedges than its lane group
+        // one window into this CTA's chunk of S_{i+1} / P_{i+1}
+        auto put_at = [&](bool sel, unsigned int k, const Win &c) {
+            if (k < ch) store_win(sel ? Sn : Pn, (unsigned long long)b * ch + k, c);
+            else atomicExch(&ctrl->error, ERR_OVERFLOW);
+        };
+        // rare paths (divergent): one shared atomic per window
         auto put_direct = [&](const Win &c) {
             const bool sel = c.key <= tn;
-            unsigned long long si = warp_alloc(&nxt.nS, sel);
-            unsigned long long pi = warp_alloc(&nxt.nP, !sel);
             lsd.add(ST_STORED);
-            if (sel) {
-                if ((long long)si < p.cap) store_win(Sn, si, c);
-                else atomicExch(&ctrl->error, ERR_OVERFLOW);
-                atomicMax(&s_smax, (unsigned long long)__double_as_longlong(c.key));
-            } else {
-                if ((long long)pi < p.cap) store_win(Pn, pi, c);
-                else atomicExch(&ctrl->error, ERR_OVERFLOW);
-                atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(c.key));
-            }
+            put_at(sel, atomicAdd(&s_n[sel ? 0 : 1], 1u), c);
+            if (sel) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(c.key));
+            else atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(c.key));
         };
 
         // warp work items: S_i windows (32 per warp), fan candidates of i-1
-        // (one per warp), P_i windows (32 per warp)
-        const unsigned long long nwS = (nS + 31) >> 5, nwP = (nP + 31) >> 5;
-        const unsigned long long nwF = (nF + FANS_PER_WARP - 1) / FANS_PER_WARP;
-        const unsigned long long W = nwS + nwF + nwP;
-        // counts stay far below 2^32: 32-bit division (a 64-bit one is a
-        // software routine on the critical path of every iteration)
-        const unsigned int trips = ((unsigned int)W + (unsigned int)nwarps - 1u) / (unsigned int)nwarps;
-        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_TRIP0);
-        for (unsigned int tr = 0; tr < trips; ++tr) {
-            const unsigned long long wi = tr * nwarps + gwid;
+        // (FANS_PER_WARP per warp), P_i windows (32 per warp); warps run
+        // independently, no CTA-wide synchronisation until the iteration end
+        const unsigned int nwS = (nS + 31u) >> 5, nwP = (nP + 31u) >> 5;
+        const unsigned int nwF = (nF + FANS_PER_WARP - 1u) / FANS_PER_WARP;
+        const unsigned int W = nwS + nwF + nwP;
+        for (unsigned int wi = (unsigned int)gwid; wi < W; wi += (unsigned int)nwarps) {
             Win o0, o1, o2;   // o2: a sibling left behind by chaining
             int no = 0;
             bool h2 = false;
             if (wi < nwS) {
-                const unsigned long long i = (wi << 5) + lane;
+                const unsigned int i = (wi << 5) + lane;
                 if (i < nS) {
                     long long c0 = p.prof ? clock64() : 0;
-                    Win win = load_win(Sc, i);
-                    if (p.trace && tr == 0) {
-                        asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
-                        atomicMax(&s_tl, globaltimer());
-                    }
+                    Win win = load_win(Sc, chunk_slot(s_pre[0], G, i, ch));
                     long long c1 = 0;
                     if (p.prof) {
                         asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
@@ -1304,18 +1378,17 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
                     }
                     // chaining: a child that the next batch would select
                     // (key <= t_{i+1}) is propagated right away by the same
-                    // thread, up to p.chain propagations; its sibling is
-                    // routed directly
+                    // thread, up to p.chain propagations
                     for (int step = 1;; ++step) {
-                        no = propagate(p, sg, it, &cur.nF, p.fanev[it & 1], win, o0, o1, ls);
+                        no = propagate(p, sg, it, fsink, win, o0, o1, ls);
                         if (no > maxchild) maxchild = no;
                         if (step >= p.chain || no == 0) break;
                         const bool c0ok = o0.key <= tn, c1ok = no > 1 && o1.key <= tn;
                         if (!c0ok && !c1ok) break;
                         const bool take1 = c1ok && (!c0ok || o1.key < o0.key);
                         if (no > 1) {
-                            // the child not chained: routed with the trip's
-                            // scan (first one) or directly (chain > 2)
+                            // the child not chained: routed with the warp's
+                            // outputs (first one) or directly (chain > 2)
                             if (!h2) {
                                 o2 = take1 ? o0 : o1;
                                 h2 = true;
@@ -1336,11 +1409,10 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
                 }
             } else if (wi < nwS + nwF) {
                 // FANS_PER_WARP candidates per warp, FAN_LANES lanes each
-                long long c3 = p.prof ? clock64() : 0;
-                const unsigned long long fi = (wi - nwS) * FANS_PER_WARP + lane / FAN_LANES;
+                const unsigned int fi = (wi - nwS) * FANS_PER_WARP + lane / FAN_LANES;
                 const int sl = lane % FAN_LANES;
                 if (fi < nF) {
-                    const FanEv e = fev[fi];
+                    const FanEv e = fev[chunk_slot(s_pre[2], G, fi, chF)];
                     const RowTabs T = row_tabs(p, e.row, it);
                     const unsigned long long dv = __ldcg(T.dist + e.v);
                     const ulonglong2 pk = __ldcg(T.pick + e.v);
@@ -1363,118 +1435,84 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
                             fan_item(p, T, e.row, e.cand, f, q % f.m, q / f.m, false, put_direct, lsd);
                     }
                 }
-                if (p.prof) {
-                    ls.add(ST_CYC_FANITEM, clock64() - c3);
-                    ls.add(ST_N_FANITEM);
-                }
-            } else if (wi < W) {
-                const unsigned long long i = ((wi - nwS - nwF) << 5) + lane;
+            } else {
+                const unsigned int i = ((wi - nwS - nwF) << 5) + lane;
                 if (i < nP) {
-                    o0 = load_win(Pc, i);
+                    o0 = load_win(Pc, chunk_slot(s_pre[1], G, i, ch));
                     no = 1;
                 }
             }
-            if (p.trace && tr == 0) {
-                // latest end of the first trip's work over the grid (S
-                // windows) and of the fan warps (TR_FAN_END)
-                unsigned long long now = globaltimer();
-                if (wi < nwS) atomicMax(&s_tw, now);
-                else if (wi < nwS + nwF) atomicMax(&s_tf, now);
-            }
             // route: S_{i+1} if key <= t_{i+1}, else P_{i+1}
-            long long c2 = p.prof ? clock64() : 0;
+            __syncwarp();
             const bool s0 = no > 0 && o0.key <= tn, s1 = no > 1 && o1.key <= tn;
             const bool k0 = no > 0 && !s0, k1 = no > 1 && !s1;
             const bool s2 = h2 && o2.key <= tn, k2 = h2 && !s2;
             const unsigned int ns_ = (unsigned int)s0 + (unsigned int)s1 + (unsigned int)s2;
             const unsigned int np_ = (unsigned int)k0 + (unsigned int)k1 + (unsigned int)k2;
-            if (k0) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o0.key));
-            if (k1) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o1.key));
-            if (k2) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(o2.key));
-            if (s0) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o0.key));
-            if (s1) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o1.key));
-            if (s2) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(o2.key));
-            unsigned int tot;
-            const unsigned int ex = block_excl_scan(ns_ | (np_ << 16), tot);
-            if (threadIdx.x == 0) {
-                s_res[0] = (tot & 0xffffu) ? atomicAdd(&nxt.nS, (unsigned long long)(tot & 0xffffu)) : 0ull;
-                s_res[1] = (tot >> 16) ? atomicAdd(&nxt.nP, (unsigned long long)(tot >> 16)) : 0ull;
-                s_res[2] = sg.nfe ? atomicAdd(&cur.nF, (unsigned long long)min(sg.nfe, (unsigned int)FE_CAP)) : 0ull;
+            // warp-reduced key extremes, one shared atomic per warp
+            double kmin = k0 ? o0.key : INFINITY, kmax = s0 ? o0.key : 0.0;
+            if (k1) kmin = fmin(kmin, o1.key);
+            if (k2) kmin = fmin(kmin, o2.key);
+            if (s1) kmax = fmax(kmax, o1.key);
+            if (s2) kmax = fmax(kmax, o2.key);
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                kmin = fmin(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+                kmax = fmax(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
             }
-            __syncthreads();
-            if (p.trace && tr == 0 && threadIdx.x == 0) {
-                trace_max(p, it, TR_SCAN_END);
-                if (it < p.trace_cap) {
-                    atomicMax(p.trace + (size_t)it * TR_N + TR_WORK_END, s_tw);
-                    atomicMax(p.trace + (size_t)it * TR_N + TR_LOADED, s_tl);
-                    atomicMax(p.trace + (size_t)it * TR_N + TR_FAN_END, s_tf);
-                }
-                s_tw = s_tl = s_tf = 0ull;
+            if (lane == 0) {
+                if (kmin < INFINITY) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(kmin));
+                if (kmax > 0.0) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(kmax));
             }
-            unsigned long long sa = s_res[0] + (ex & 0xffffu), pa = s_res[1] + (ex >> 16);
-            if (no > 0) {
-                if (s0) put(Sn, sa++, o0);
-                else put(Pn, pa++, o0);
-            }
-            if (no > 1) {
-                if (s1) put(Sn, sa++, o1);
-                else put(Pn, pa++, o1);
-            }
-            if (h2) {
-                if (s2) put(Sn, sa, o2);
-                else put(Pn, pa, o2);
-            }
-            const unsigned int nfe = min(sg.nfe, (unsigned int)FE_CAP);
-            FanEv *fout = p.fanev[it & 1];
-            for (unsigned int k = threadIdx.x; k < nfe; k += TPB) {
-                unsigned long long at = s_res[2] + k;
-                if ((long long)at < p.fancap) fout[at] = sg.fe[k];
-                else atomicExch(&ctrl->error, ERR_OVERFLOW);
-            }
-            if (++trips_since_fold == FOLD_TRIPS) {
+            unsigned int sa = warp_chunk_alloc(&s_n[0], ns_);
+            unsigned int pa = warp_chunk_alloc(&s_n[1], np_);
+            if (no > 0) put_at(s0, s0 ? sa++ : pa++, o0);
+            if (no > 1) put_at(s1, s1 ? sa++ : pa++, o1);
+            if (h2) put_at(s2, s2 ? sa : pa, o2);
+            ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
+            if (++iters_since_fold == FOLD_TRIPS) {
                 ls.fold();
-                trips_since_fold = 0;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) sg.nfe = 0u;
-            __syncthreads();
-            if (p.prof && no > 0) {
-                ls.add(ST_CYC_POOL, clock64() - c2);
-                ls.add(ST_N_POOL);
+                iters_since_fold = 0;
             }
         }
+        // publish this CTA's outputs, then the grid barrier
+        __syncthreads();
         if (threadIdx.x == 0) {
+            const int po = par ^ 1;  // parity of the next iteration's inputs
+            p.ccnt[(size_t)(po * 3 + 0) * MAX_CTAS + b] = min(s_n[0], (unsigned int)ch);
+            p.ccnt[(size_t)(po * 3 + 1) * MAX_CTAS + b] = min(s_n[1], (unsigned int)ch);
+            p.ccnt[(size_t)(par * 3 + 2) * MAX_CTAS + b] = min(s_n[2], (unsigned int)chF);
+            s_n[0] = s_n[1] = s_n[2] = 0u;
             if (s_pmin != ~0ull) atomicMin(&nxt.pmin, s_pmin);
             if (s_smax) atomicMax(&nxt.smax, s_smax);
             s_pmin = ~0ull;
             s_smax = 0ull;
             if (p.trace) trace_max(p, it, TR_A_END);
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            if (p.max_iter > 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
-            if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
+            if (blockIdx.x == 0) {
+                if (p.max_iter > 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
+                if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
+            }
         }
         grid_barrier(ctrl, gen, [&] {
             s_c[0] = (unsigned long long)*(volatile int *)&ctrl->error;
-            s_c[1] = *(volatile unsigned long long *)&nxt.nS;
-            s_c[2] = *(volatile unsigned long long *)&nxt.nP;
-            s_c[3] = *(volatile unsigned long long *)&cur.nF;
-            s_c[4] = *(volatile unsigned long long *)&nxt.pmin;
-            s_c[5] = *(volatile unsigned long long *)&nxt.smax;
+            s_c[1] = *(volatile unsigned long long *)&nxt.pmin;
+            s_c[2] = *(volatile unsigned long long *)&nxt.smax;
         });
+        // the next iteration's inputs: S_{i+1}, P_{i+1} (parity par^1) and
+        // the fan candidates of iteration i (parity par)
+        build_prefix(par ^ 1, par);
         const int err = (int)s_c[0];
-        const unsigned long long ns = s_c[1];
-        const unsigned long long np = s_c[2];
-        const unsigned long long nf = s_c[3];
+        const unsigned int ns = s_pre[0][G], np = s_pre[1][G], nf = s_pre[2][G];
         if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *trr = p.trace + (size_t)it * TR_N;
             trr[TR_B1] = trr[TR_B_END] = trr[TR_B2] = globaltimer();
-            trr[TR_NC] = ns + np;
+            trr[TR_NC] = (unsigned long long)ns + np;
         }
         ++it;
         if (err || (ns == 0 && np == 0 && nf == 0)) break;
         t = tn;
     }
+    __syncwarp();
     ls.fold();
     if (maxchild) ls.max(ST_MAXCHILD, maxchild);
     flush_stats(ctrl, s_st);
@@ -1529,10 +1567,21 @@ __global__ void k_source_windows(Params p, const int64_t *src, int nsrc) {
     LocalStats ls{s_st, true};
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     Ctrl *ctrl = p.ctrl;
+    // the live solver reads its batch in per-CTA chunks: source i seeds
+    // chunk i % G (G = the solver's grid); the deterministic one linearly
+    const unsigned long long G = (unsigned long long)p.live_grid;
+    const unsigned long long ch = G ? (unsigned long long)p.cap / G : 0ull;
     auto emit = [&](const Win &c) {
-        unsigned long long slot = atomicAdd(&ctrl->slot[0].nS, 1ull);
-        if ((long long)slot < p.cap) store_win(p.S, slot, c);
-        else atomicExch(&ctrl->error, ERR_OVERFLOW);
+        if (p.live) {
+            const unsigned long long c0 = (unsigned long long)i % G;
+            const unsigned int k = atomicAdd(p.ccnt + c0, 1u);  // parity 0, S counts
+            if (k < ch) store_win(p.S, c0 * ch + k, c);
+            else atomicExch(&ctrl->error, ERR_OVERFLOW);
+        } else {
+            unsigned long long slot = atomicAdd(&ctrl->slot[0].nS, 1ull);
+            if ((long long)slot < p.cap) store_win(p.S, slot, c);
+            else atomicExch(&ctrl->error, ERR_OVERFLOW);
+        }
         ls.add(ST_STORED);
     };
     if (i < nsrc) {
@@ -1670,6 +1719,7 @@ static int ensure_ws(pch_mesh *m, long long cap, int rows) {
     if ((rc = ws_alloc(m, &p.hist[0], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.hist[1], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.ctrl, 1))) return rc;
+    if ((rc = ws_alloc(m, &p.ccnt, 2 * 3 * MAX_CTAS))) return rc;
     p.cap = cap;
     m->cap = cap;
     m->rows_alloc = rows;
@@ -1734,6 +1784,9 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         if (p.trace) CK(cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * TR_N * p.trace_cap, st));
         CK(cudaEventRecord(m->ev0, st));
         CK(cudaMemsetAsync(p.ctrl, 0, sizeof(Ctrl), st));
+        const bool wide = rows >= WIDE_ROWS && m->grid_live2 > 0;
+        p.live_grid = wide ? m->grid_live2 : m->grid_live;
+        if (p.live) CK(cudaMemsetAsync(p.ccnt, 0, sizeof(unsigned int) * 2 * 3 * MAX_CTAS, st));
         k_init_state<<<4 * 148, 256, 0, st>>>(p, d_src, nsrc);
         CK(cudaGetLastError());
         k_set_sources<<<(nsrc + 255) / 256, 256, 0, st>>>(p, d_src, nsrc);
@@ -1744,10 +1797,8 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         void *args[] = {&p};
         if (p.live)
         {
-            const bool wide = rows >= WIDE_ROWS && m->grid_live2 > 0;
             const void *kern = wide ? (const void *)pch_live<2> : (const void *)pch_live<1>;
-            CK(cudaLaunchCooperativeKernel(kern, dim3(wide ? m->grid_live2 : m->grid_live), dim3(TPB), args,
-                                           0, st));
+            CK(cudaLaunchCooperativeKernel(kern, dim3(p.live_grid), dim3(TPB), args, 0, st));
         }
         else
             CK(cudaLaunchCooperativeKernel((const void *)pch_persistent, dim3(m->grid), dim3(TPB), args, 0, st));

@@ -380,6 +380,18 @@ __device__ __forceinline__ void dist_event(const Params &p, const RowTabs &t, St
 __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, Stage &sg, int32_t j,
                                             double comp, double entry, ulonglong2 guess, LocalStats &ls) {
     ls.add(ST_EV_CREATED);
+    if (p.live) {
+        // live solver: one CAS attempt, reply unused (off the propagation's
+        // critical path).  A lost race leaves the entry at a value that is
+        // still smaller than the one read -- a window that kept both its
+        // children -- so it is a valid dominator for the one-angle-one-split
+        // rule; losing only weakens pruning, never correctness.
+        if (ord64(comp) < guess.x || (ord64(comp) == guess.x && ord64(entry) < guess.y)) {
+            atomicCAS(t.split + j, guess, make_ulonglong2(ord64(comp), ord64(entry)));
+            ls.add(ST_EV_APPLIED);
+        }
+        return;
+    }
     int tries = 0;
     const bool won = cas_min_u128(t.split + j, ord64(comp), ord64(entry), guess, &tries);
     if (p.prof) {

@@ -407,10 +407,26 @@ __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, S
     }
 }
 
+// A fan-pick claim whose first CAS attempt is in flight: the live solver
+// issues it during the propagation and completes it (retrying if the pick
+// moved) after the window's children are routed, so the round trip
+// overlaps that work.  One per thread; further claims are synchronous.
+struct FanPend {
+    ulonglong2 *ptr;
+    ulonglong2 guess, want, seen;
+    bool active;
+    bool enabled;
+    __device__ __forceinline__ void complete() {
+        if (!active) return;
+        active = false;
+        if (seen.x != guess.x || seen.y != guess.y) cas_min_u128(ptr, want.x, want.y, seen);
+    }
+};
+
 template <typename FanSink>
 __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uint32_t row, FanSink &&sink,
-                                          ulonglong2 guess, int32_t v, int32_t anchor, double cand,
-                                          double ax, double ay, double bx, double by) {
+                                          FanPend &pend, ulonglong2 guess, int32_t v, int32_t anchor,
+                                          double cand, double ax, double ay, double bx, double by) {
     FanEv e;
     e.v = v;
     e.row = row;
@@ -430,11 +446,21 @@ __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uin
     // CAS with the pick it read, so a claim is one round trip.
     const unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
     const unsigned long long lo = fan_tiebreak(e);
-    int tries = 0;
-    cas_min_u128(t.pick + v, hi, lo, guess, &tries);
-    if (p.prof) {
-        atomicAdd(&p.ctrl->st[ST_CAS_FAN_CALLS], 1ull);
-        atomicAdd(&p.ctrl->st[ST_CAS_FAN_TRIES], (unsigned long long)tries);
+    if (pend.enabled && !pend.active) {
+        if (hi < guess.x || (hi == guess.x && lo < guess.y)) {
+            pend.ptr = t.pick + v;
+            pend.guess = guess;
+            pend.want = make_ulonglong2(hi, lo);
+            pend.seen = atomicCAS(pend.ptr, guess, pend.want);
+            pend.active = true;
+        }
+    } else {
+        int tries = 0;
+        cas_min_u128(t.pick + v, hi, lo, guess, &tries);
+        if (p.prof) {
+            atomicAdd(&p.ctrl->st[ST_CAS_FAN_CALLS], 1ull);
+            atomicAdd(&p.ctrl->st[ST_CAS_FAN_TRIES], (unsigned long long)tries);
+        }
     }
     sink(e);
 }
@@ -652,7 +678,7 @@ __device__ void emit_fan(const Params &p, const RowTabs &t, uint32_t row, int32_
 // Up to two children are returned in `c`; events go to the shadow tables.
 
 template <typename FanSink>
-__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, FanSink &&fsink,
+__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, FanSink &&fsink, FanPend &pend,
                                          const Win &w, Win &out0, Win &out1, LocalStats &ls) {
     // Latency layout: the per-iteration critical path is one propagation
     // (of the slowest lane of the slowest warp), so
@@ -797,13 +823,13 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     if (claim) angle_event(p, T, sg, j, comp, entry_x, sp_raw, ls);
     // saddle fans (Fig. 3c): the reverse direction of the incoming ray
     // relative to an anchor half-edge out of the vertex (geom.py:353-484)
-    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, fsink, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
+    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, fsink, pend, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
     if (ev1 && (v1f & SADDLE_BIT)) {
         if (far) {
             // anchor jo = v1 -> v0: its wedge follows next(j)'s, so this is
             // the reference's anchor next(j) with the corner at v1 folded
             // into the anchor angle
-            fan_event(p, T, w.row, fsink, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
+            fan_event(p, T, w.row, fsink, pend, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
         } else {
             // boundary window: anchor next(j), the source-side apex
             // direction from v1 (geom.py:372-377)
@@ -814,12 +840,12 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
             const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
             const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
             const double ay2 = lps * lps - axs * axs;
-            fan_event(p, T, w.row, fsink, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
+            fan_event(p, T, w.row, fsink, pend, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
                       ay2 > 0.0 ? sqrt(ay2) : 0.0);
         }
     }
     if (evd && (vdf & SADDLE_BIT))
-        fan_event(p, T, w.row, fsink, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
+        fan_event(p, T, w.row, fsink, pend, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
     return nc;
 }
 
@@ -1004,7 +1030,10 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 if (i < nS) {
                     long long c0 = p.prof ? clock64() : 0;
                     Win win = load_win(p.S, i);
-                    nc = propagate(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, win, ca, cb, ls);
+                    FanPend sync_pend{};
+                    sync_pend.enabled = false;
+                    nc = propagate(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, sync_pend, win, ca,
+                                   cb, ls);
                     if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
                     if (nc > maxchild) maxchild = nc;
                 }
@@ -1378,6 +1407,8 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
             Win o0, o1, o2;   // o2: a sibling left behind by chaining
             int no = 0;
             bool h2 = false;
+            FanPend pend{};
+            pend.enabled = true;
             if (wi < nwS) {
                 const unsigned int i = (wi << 5) + lane;
                 if (i < nS) {
@@ -1392,7 +1423,7 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
                     // (key <= t_{i+1}) is propagated right away by the same
                     // thread, up to p.chain propagations
                     for (int step = 1;; ++step) {
-                        no = propagate(p, sg, it, fsink, win, o0, o1, ls);
+                        no = propagate(p, sg, it, fsink, pend, win, o0, o1, ls);
                         if (no > maxchild) maxchild = no;
                         if (step >= p.chain || no == 0) break;
                         const bool c0ok = o0.key <= tn, c1ok = no > 1 && o1.key <= tn;
@@ -1482,6 +1513,7 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
             if (no > 1) put_at(s1, s1 ? sa++ : pa++, o1);
             if (h2) put_at(s2, s2 ? sa : pa, o2);
             ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
+            pend.complete();
             if (++iters_since_fold == FOLD_TRIPS) {
                 ls.fold();
                 iters_since_fold = 0;

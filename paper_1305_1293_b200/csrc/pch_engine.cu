@@ -1224,17 +1224,17 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
 // 2 for batched rows (throughput bound: twice the warps per SM hide the
 // chain's latency, at the price of a few register spills)
 // Item index -> slot of a chunked buffer: chunk c holds items
-// [pre[c], pre[c+1]) at slots c * ch + (i - pre[c]) (binary search over the
-// CTA prefix table in shared memory).
+// [pre[c], pre[c+1]) at slots c * ch + (i - pre[c]).  Chunks are filled
+// about evenly (windows are spread over the CTAs), so the search starts at
+// the proportional guess i * G / n and walks at most a few chunks.
 __device__ __forceinline__ unsigned long long chunk_slot(const unsigned int *pre, int G, unsigned int i,
                                                          unsigned long long ch) {
-    int lo = 0, hi = G;
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (pre[mid] <= i) lo = mid;
-        else hi = mid;
-    }
-    return (unsigned long long)lo * ch + (i - pre[lo]);
+    const unsigned int n = pre[G];
+    int c = (int)(((unsigned long long)i * (unsigned)G) / (n ? n : 1u));
+    c = c < G - 1 ? c : G - 1;
+    while (c > 0 && pre[c] > i) --c;
+    while (c < G - 1 && pre[c + 1] <= i) ++c;
+    return (unsigned long long)c * ch + (i - pre[c]);
 }
 
 // warp-level reservation in the CTA's own chunk: every lane brings `n`

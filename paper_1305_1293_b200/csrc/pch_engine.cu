@@ -931,6 +931,13 @@ __device__ __forceinline__ void trace_max(const Params &p, int it, int slot) {
     if (p.trace && it < p.trace_cap) atomicMax(p.trace + (size_t)it * TR_N + slot, globaltimer());
 }
 
+// one trace stamp per warp (the first active lane): per-lane global
+// atomics on one address would serialise and distort the timeline
+__device__ __forceinline__ void trace_max_warp(const Params &p, int it, int slot) {
+    const unsigned m = __activemask();
+    if ((threadIdx.x & 31) == __ffs(m) - 1) trace_max(p, it, slot);
+}
+
 // CTA-level allocation of `n` (<= 3) pool slots per thread for one trip:
 // one global atomicAdd per CTA; returns the thread's first slot index
 // relative to the counter (uniform: contains __syncthreads)
@@ -1237,22 +1244,28 @@ __device__ __forceinline__ unsigned long long chunk_slot(const unsigned int *pre
     return (unsigned long long)c * ch + (i - pre[c]);
 }
 
-// warp-level reservation in the CTA's own chunk: every lane brings `n`
-// items, gets its first slot index (relative to the chunk); one shared
-// atomic per warp (converged warp)
-__device__ __forceinline__ unsigned int warp_chunk_alloc(unsigned int *s_cnt, unsigned int n) {
+// warp-level reservation in the CTA's own chunks of S_{i+1} and P_{i+1}:
+// every lane brings ns / np items (< 2^16 per warp), one packed scan and
+// one shared 64-bit atomic per warp (S count in the low, P in the high
+// half); returns the lane's first slot in each chunk (converged warp)
+__device__ __forceinline__ void warp_chunk_alloc2(unsigned long long *s_cnt, unsigned int ns, unsigned int np,
+                                                  unsigned int &sa, unsigned int &pa) {
     const int lane = threadIdx.x & 31;
+    const unsigned int n = ns | (np << 16);
     unsigned int x = n;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
         if (lane >= o) x += y;
     }
-    const unsigned int total = __shfl_sync(0xffffffffu, x, 31);
-    unsigned int base = 0;
-    if (lane == 31 && total) base = atomicAdd(s_cnt, total);
+    const unsigned int tot = __shfl_sync(0xffffffffu, x, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && tot)
+        base = atomicAdd(s_cnt, (unsigned long long)(tot & 0xffffu) | ((unsigned long long)(tot >> 16) << 32));
     base = __shfl_sync(0xffffffffu, base, 31);
-    return base + x - n;
+    const unsigned int ex = x - n;
+    sa = (unsigned int)base + (ex & 0xffffu);
+    pa = (unsigned int)(base >> 32) + (ex >> 16);
 }
 
 // MINB = resident CTAs per SM the register budget targets: 1 for single
@@ -1274,7 +1287,8 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
     __shared__ unsigned long long s_st[N_ST];
     __shared__ Stage sg;                        // unused staging (shared helpers)
     __shared__ unsigned int s_pre[3][MAX_CTAS + 1];  // prefix tables: S, P, fans(prev)
-    __shared__ unsigned int s_n[3];             // this CTA's outputs: S, P, fans
+    __shared__ unsigned long long s_nsp;        // this CTA's outputs: S (low) / P (high)
+    __shared__ unsigned int s_nf;               // this CTA's fan candidates
     __shared__ unsigned long long s_pmin, s_smax;
     __shared__ unsigned long long s_c[3];       // err, pmin, smax of the finished iteration
     stats_init(s_st);
@@ -1282,7 +1296,8 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
         sg.ntv = sg.nte = sg.nfe = 0u;
         s_pmin = ~0ull;
         s_smax = 0ull;
-        s_n[0] = s_n[1] = s_n[2] = 0u;
+        s_nsp = 0ull;
+        s_nf = 0u;
     }
     LocalStats ls{s_st, false};   // packed per-thread counters, folded every FOLD_TRIPS
     LocalStats lsd{s_st, true};   // rare paths: straight to shared memory
@@ -1379,7 +1394,7 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
         }
         // fan candidates of this iteration go straight to the CTA's chunk
         auto fsink = [&](const FanEv &e) {
-            const unsigned int k = atomicAdd(&s_n[2], 1u);
+            const unsigned int k = atomicAdd(&s_nf, 1u);
             if (k < chF) fout[k] = e;
             else atomicExch(&ctrl->error, ERR_OVERFLOW);
         };
@@ -1392,7 +1407,8 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
         auto put_direct = [&](const Win &c) {
             const bool sel = c.key <= tn;
             lsd.add(ST_STORED);
-            put_at(sel, atomicAdd(&s_n[sel ? 0 : 1], 1u), c);
+            const unsigned long long old = atomicAdd(&s_nsp, sel ? 1ull : (1ull << 32));
+            put_at(sel, sel ? (unsigned int)old : (unsigned int)(old >> 32), c);
             if (sel) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(c.key));
             else atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(c.key));
         };
@@ -1413,7 +1429,16 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
                 const unsigned int i = (wi << 5) + lane;
                 if (i < nS) {
                     long long c0 = p.prof ? clock64() : 0;
-                    Win win = load_win(Sc, chunk_slot(s_pre[0], G, i, ch));
+                    const unsigned long long slot0 = chunk_slot(s_pre[0], G, i, ch);
+                    if (p.trace) {
+                        asm volatile("" ::"l"(slot0));
+                        trace_max_warp(p, it, TR_TRIP0);
+                    }
+                    Win win = load_win(Sc, slot0);
+                    if (p.trace) {
+                        asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
+                        trace_max_warp(p, it, TR_LOADED);
+                    }
                     long long c1 = 0;
                     if (p.prof) {
                         asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
@@ -1441,6 +1466,10 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
                         }
                         win = take1 ? o1 : o0;
                         no = 0;
+                    }
+                    if (p.trace) {
+                        asm volatile("" ::"d"((no > 0 ? o0.key : 0.0) + (no > 1 ? o1.key : 0.0)));
+                        trace_max_warp(p, it, TR_WORK_END);
                     }
                     if (p.prof) {
                         asm volatile("" ::"d"((no > 0 ? o0.key : 0.0) + (no > 1 ? o1.key : 0.0)));
@@ -1492,28 +1521,32 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
             const bool s2 = h2 && o2.key <= tn, k2 = h2 && !s2;
             const unsigned int ns_ = (unsigned int)s0 + (unsigned int)s1 + (unsigned int)s2;
             const unsigned int np_ = (unsigned int)k0 + (unsigned int)k1 + (unsigned int)k2;
-            // warp-reduced key extremes, one shared atomic per warp
-            double kmin = k0 ? o0.key : INFINITY, kmax = s0 ? o0.key : 0.0;
-            if (k1) kmin = fmin(kmin, o1.key);
-            if (k2) kmin = fmin(kmin, o2.key);
-            if (s1) kmax = fmax(kmax, o1.key);
-            if (s2) kmax = fmax(kmax, o2.key);
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                kmin = fmin(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
-                kmax = fmax(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
-            }
+            // warp-reduced key extremes on the top 32 bits of the (positive,
+            // order-preserving) fp64 patterns, one shared atomic per warp:
+            // the pool minimum rounds down, the batch maximum up -- both
+            // only steer the controller
+            const auto hi32 = [](double x) {
+                return (unsigned int)((unsigned long long)__double_as_longlong(x) >> 32);
+            };
+            unsigned int hmin = k0 ? hi32(o0.key) : 0xffffffffu, hmax = s0 ? hi32(o0.key) : 0u;
+            if (k1) hmin = min(hmin, hi32(o1.key));
+            if (k2) hmin = min(hmin, hi32(o2.key));
+            if (s1) hmax = max(hmax, hi32(o1.key));
+            if (s2) hmax = max(hmax, hi32(o2.key));
+            hmin = __reduce_min_sync(0xffffffffu, hmin);
+            hmax = __reduce_max_sync(0xffffffffu, hmax);
             if (lane == 0) {
-                if (kmin < INFINITY) atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(kmin));
-                if (kmax > 0.0) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(kmax));
+                if (hmin != 0xffffffffu) atomicMin(&s_pmin, (unsigned long long)hmin << 32);
+                if (hmax) atomicMax(&s_smax, ((unsigned long long)hmax << 32) | 0xffffffffull);
             }
-            unsigned int sa = warp_chunk_alloc(&s_n[0], ns_);
-            unsigned int pa = warp_chunk_alloc(&s_n[1], np_);
+            unsigned int sa, pa;
+            warp_chunk_alloc2(&s_nsp, ns_, np_, sa, pa);
             if (no > 0) put_at(s0, s0 ? sa++ : pa++, o0);
             if (no > 1) put_at(s1, s1 ? sa++ : pa++, o1);
             if (h2) put_at(s2, s2 ? sa : pa, o2);
             ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
             pend.complete();
+            if (p.trace && wi < nwS) trace_max_warp(p, it, TR_SCAN_END);
             if (++iters_since_fold == FOLD_TRIPS) {
                 ls.fold();
                 iters_since_fold = 0;
@@ -1523,10 +1556,11 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
         __syncthreads();
         if (threadIdx.x == 0) {
             const int po = par ^ 1;  // parity of the next iteration's inputs
-            p.ccnt[(size_t)(po * 3 + 0) * MAX_CTAS + b] = min(s_n[0], (unsigned int)ch);
-            p.ccnt[(size_t)(po * 3 + 1) * MAX_CTAS + b] = min(s_n[1], (unsigned int)ch);
-            p.ccnt[(size_t)(par * 3 + 2) * MAX_CTAS + b] = min(s_n[2], (unsigned int)chF);
-            s_n[0] = s_n[1] = s_n[2] = 0u;
+            p.ccnt[(size_t)(po * 3 + 0) * MAX_CTAS + b] = min((unsigned int)s_nsp, (unsigned int)ch);
+            p.ccnt[(size_t)(po * 3 + 1) * MAX_CTAS + b] = min((unsigned int)(s_nsp >> 32), (unsigned int)ch);
+            p.ccnt[(size_t)(par * 3 + 2) * MAX_CTAS + b] = min(s_nf, (unsigned int)chF);
+            s_nsp = 0ull;
+            s_nf = 0u;
             if (s_pmin != ~0ull) atomicMin(&nxt.pmin, s_pmin);
             if (s_smax) atomicMax(&nxt.smax, s_smax);
             s_pmin = ~0ull;

@@ -50,6 +50,12 @@ def trace_summary(path):
           f"nP mean={a[:, 6].mean():.0f} nC mean={a[:, 7].mean():.0f} nF mean={a[:, 8].mean():.0f} "
           f"fan-phase={fan/len(a):.1f}us/iter", flush=True)
     sm, we, se = a[:, 12], a[:, 13], a[:, 14]
+    t0m, ld = a[:, 15], a[:, 16]
+    okl = (t0m > 0) & (ld > 0) & (we > 0) & (se > 0)
+    if okl.any():
+        print(f"   live path (max over warps, from t0): item start {np.mean(t0m[okl] - t0[okl])/1e3:.2f}us "
+              f"window loaded {np.mean(ld[okl] - t0[okl])/1e3:.2f}us propagated {np.mean(we[okl] - t0[okl])/1e3:.2f}us "
+              f"routed {np.mean(se[okl] - t0[okl])/1e3:.2f}us A end {np.mean(ae[okl] - t0[okl])/1e3:.2f}us", flush=True)
     ok = (sm > 0) & (we > 0) & (se > 0)
     if ok.any():
         print(f"   live split per iter: start-skew={np.mean(sm[ok] - t0[ok])/1e3:.2f}us "

@@ -1237,7 +1237,8 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
 __device__ __forceinline__ unsigned long long chunk_slot(const unsigned int *pre, int G, unsigned int i,
                                                          unsigned long long ch) {
     const unsigned int n = pre[G];
-    int c = (int)(((unsigned long long)i * (unsigned)G) / (n ? n : 1u));
+    // fp32 guess: a 64-bit integer division is a long software sequence
+    int c = (int)((float)i * __frcp_rn((float)(n ? n : 1u)) * (float)G);
     c = c < G - 1 ? c : G - 1;
     while (c > 0 && pre[c] > i) --c;
     while (c < G - 1 && pre[c + 1] <= i) ++c;
@@ -1384,6 +1385,7 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
             clr.smax = 0ull;
             ls.max(ST_PEAK, (unsigned long long)nS + nP);
         }
+        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_START_MAX);
         if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *tr = p.trace + (size_t)it * TR_N;
             tr[TR_T0] = globaltimer();

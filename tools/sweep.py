@@ -53,7 +53,8 @@ def trace_summary(path):
     t0m, ld = a[:, 15], a[:, 16]
     okl = (t0m > 0) & (ld > 0) & (we > 0) & (se > 0)
     if okl.any():
-        print(f"   live path (max over warps, from t0): item start {np.mean(t0m[okl] - t0[okl])/1e3:.2f}us "
+        print(f"   live path (max over warps, from t0): CTA start {np.mean(sm[okl] - t0[okl])/1e3:.2f}us "
+              f"item start {np.mean(t0m[okl] - t0[okl])/1e3:.2f}us "
               f"window loaded {np.mean(ld[okl] - t0[okl])/1e3:.2f}us propagated {np.mean(we[okl] - t0[okl])/1e3:.2f}us "
               f"routed {np.mean(se[okl] - t0[okl])/1e3:.2f}us A end {np.mean(ae[okl] - t0[okl])/1e3:.2f}us", flush=True)
     ok = (sm > 0) & (we > 0) & (se > 0)

@@ -1852,7 +1852,9 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             if (dlt > 0.0) p.delta_min = dlt;
         }
         p.prof = getenv("PCH_PROFILE") ? 1 : 0;
-        p.chain = cfg->chain > 0 ? cfg->chain : DEFAULT_CHAIN;
+        // chaining shortens the latency-bound single field; batched rows
+        // are throughput bound and do better without it (fewer windows)
+        p.chain = cfg->chain > 0 ? cfg->chain : (rows >= WIDE_ROWS ? 1 : DEFAULT_CHAIN);
         if (const char *ch = getenv("PCH_CHAIN")) p.chain = std::max(1, atoi(ch));  // development
         const char *trace_path = getenv("PCH_TRACE");
         if (trace_path && !m->trace) {

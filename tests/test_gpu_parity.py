@@ -191,3 +191,47 @@ def test_edge_lipschitz_and_sandwich_terrain():
     assert np.all(np.abs(d[u] - d[v]) <= m.length + 1e-9)
     chord = np.linalg.norm(m.positions - m.positions[s], axis=1)
     assert np.all(chord - 1e-9 <= d)
+
+
+@pytest.mark.parametrize("n", [5, 8, 40])
+def test_batched_rows_match_single_fields(n):
+    """pch_run_rows solves its sources in batches (one field per row, 32
+    per kernel; batches of >= 8 rows run the 2-CTA/SM instance): every row
+    equals the single-source field and the oracle."""
+    _gpu()
+    from oracle import oracle as O
+    from paper_1305_1293_b200 import run_pch, run_pch_rows
+    m, g = load_golden("bumpy_sphere20k_s3")
+    src = np.random.default_rng(n).choice(m.n_vertices, n, replace=False).tolist()
+    src[-1] = src[0]  # a duplicate source gets its own (identical) row
+    rows, st = run_pch_rows(m, src)
+    assert rows.shape == (n, m.n_vertices)
+    assert st.iterations >= 1
+    for r in (0, n // 2, n - 1):
+        single, _ = run_pch(m, [src[r]])
+        assert max_rel_dev(rows[r], single) <= TOL, r
+    ref, _ = O.run_ich(m, [src[1]])
+    assert max_rel_dev(rows[1], ref) <= TOL
+    assert max_rel_dev(rows[-1], rows[0]) <= TOL
+
+
+def test_batched_rows_deterministic_mode():
+    _gpu()
+    from paper_1305_1293_b200 import EngineConfig, run_pch_rows
+    m, g = load_golden("icosphere5120_multi16")
+    src = [int(s) for s in g["sources"][:4]]
+    a, _ = run_pch_rows(m, src, EngineConfig(deterministic=True))
+    b, _ = run_pch_rows(m, src, EngineConfig(deterministic=True))
+    assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    assert max_rel_dev(a.min(axis=0), run_pch_rows(m, src)[0].min(axis=0)) <= TOL
+
+
+def test_batched_rows_pool_regrow():
+    _gpu()
+    from paper_1305_1293_b200 import EngineConfig, run_pch, run_pch_rows
+    m, g = load_golden("bumpy_torus4800_s5")
+    src = list(range(0, 2400, 150))
+    rows, st = run_pch_rows(m, src, EngineConfig(pool_capacity=4096))
+    assert st.buffer_regrows >= 1
+    for r in (0, len(src) - 1):
+        assert max_rel_dev(rows[r], run_pch(m, [src[r]])[0]) <= TOL

@@ -77,49 +77,74 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def _traffic(workload):
-    """dram read+write bytes per launch of the solver kernel from the
-    committed ncu --set full summary, if one exists for this workload."""
+def _traffic(workload, key=""):
+    """dram read+write bytes per launch of the solver kernel (key "") or
+    its FP64 pipe utilisation (key "_fp64_pipe") from the committed
+    ncu --set full summary, if one exists for this workload."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             t = json.load(f)
-        return t.get(workload)
+        return t.get(workload + key)
     except Exception:
         return None
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+    """SM clock / throttle-reason sampling during the timed region
+    (B200_PROFILING.md clocks line).  NVML polled from a thread every 2 ms
+    (the timed region of a 10-step run is ~0.1 s, too short for
+    `nvidia-smi -lms`); nvidia-smi once if NVML is unavailable."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason bits
+    BITS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40),
+            ("sw_thermal_slowdown", 0x20), ("sw_power_cap", 0x4))
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def _poll(self):
+        import pynvml
+        h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+        smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while True:
+            sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+            r = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+            flags = ["Active" if r & bit else "Not Active" for _, bit in self.BITS]
+            self.lines.append(", ".join([str(self.index), str(sm), str(smax), "", ""] + flags))
+            if self.stop.wait(0.002):
+                return
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
         except Exception:
-            self.proc = None
+            self.thread = None
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
-        if self.proc is not None:
-            self.proc.terminate()
+        if self.thread is not None:
+            self.stop.set()
+            self.thread.join(timeout=5)
+        if not self.lines:
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"],
+                    capture_output=True, text=True, timeout=20).stdout
+                self.lines = [l for l in out.splitlines() if l.strip()]
             except Exception:
-                self.proc.kill()
-                out = ""
-            self.lines = [l for l in out.splitlines() if l.strip()]
+                self.lines = []
 
     def summary(self):
         sm, smax, reasons = [], None, set()
@@ -341,7 +366,10 @@ def run_b200(args):
                          "kernel_ms": round(k_ms, 4),
                          "kernel_share": round(kernel_share, 4),
                          "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": int(alg_bytes)},
+                         "algorithmic_bytes_per_launch": int(alg_bytes),
+                         # north star: FP64 pipe utilisation of the propagation
+                         # (ncu sm__pipe_fp64_cycles_active, same kernel)
+                         "fp64_pipe_frac": _traffic(args.workload, "_fp64_pipe")},
             "windows": {"created_per_field": created // args.steps,
                         "propagated_per_field": propagated // args.steps,
                         "stored_per_field": stored // args.steps,

@@ -1,6 +1,9 @@
 """Parameter sweep of the GPU engine on a bench mesh (development tool).
 
-    python tools/sweep.py WORKLOAD "k=65536,chain_band=4;k=65536,live=1" [--trace]
+    python tools/sweep.py WORKLOAD "k=65536,chain=3;k=16384,dmin=0.4" [--trace]
+
+(dmin / delta set the PCH_DELTA_MIN / PCH_DELTA development overrides:
+controller step floor / fixed step, in mean edge lengths.)
 
 Each configuration is run 3 times (best device time reported) and checked
 against the sequential ICH oracle (test infrastructure, checker only).
@@ -27,6 +30,11 @@ def parse(spec):
             continue
         k, v = kv.split("=")
         out[k] = float(v) if "." in v else int(v)
+    env = {}
+    for key, var in (("dmin", "PCH_DELTA_MIN"), ("delta", "PCH_DELTA"), ("tpb", "PCH_TPB")):
+        if key in out:
+            env[var] = str(out.pop(key))
+    out["_env"] = env
     for b in ("deterministic", "recheck"):
         if b in out:
             out[b] = bool(out[b])
@@ -91,6 +99,10 @@ def main():
     fin = np.isfinite(ref)
     for spec in specs:
         kw = parse(spec)
+        env = kw.pop("_env")
+        for var in ("PCH_DELTA_MIN", "PCH_DELTA"):
+            os.environ.pop(var, None)
+        os.environ.update(env)
         cfg = EngineConfig(**kw)
         best = None
         for rep in range(3):

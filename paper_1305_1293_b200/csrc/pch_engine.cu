@@ -347,7 +347,8 @@ __device__ __forceinline__ void flush_stats(Ctrl *c, unsigned long long *s) {
 #endif
 constexpr int TPB = PCH_TPB;      // threads per CTA of every solver kernel
 constexpr int NWARP = TPB / 32;
-constexpr double DELTA_FLOOR = 0.15;  // controller step floor, mean edge lengths
+constexpr double DELTA_FLOOR = 0.45;  // controller step floor, mean edge lengths
+constexpr double DELTA_CAP = 0.75;    // controller step cap, mean edge lengths
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
 constexpr int WIDE_ROWS = 8;          // from this many rows on, the 2-CTA/SM solver
@@ -1838,11 +1839,13 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.rows = rows;
         // step controller bounds (mean edge lengths): the floor keeps wide
         // wavefronts (tori, large spheres: far more than k windows per face
-        // layer) from splitting one layer over many iterations; measured
-        // best compromise over the bench meshes (profiles/r01_controller.md)
+        // layer) from splitting one layer over many iterations; the cap
+        // keeps narrow ones (terrain: fewer than k windows per layer) from
+        // selecting several layers out of order; measured over the bench
+        // meshes (profiles/r01_controller.md)
         p.delta0 = m->mean_edge;
         p.delta_min = DELTA_FLOOR * m->mean_edge;
-        p.delta_max = 1e3 * m->mean_edge;
+        p.delta_max = DELTA_CAP * m->mean_edge;
         if (const char *fd = getenv("PCH_DELTA")) {  // development: fixed step
             const double dlt = atof(fd) * m->mean_edge;
             if (dlt > 0.0) p.delta0 = p.delta_min = p.delta_max = dlt;
@@ -1851,6 +1854,11 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             const double dlt = atof(fm) * m->mean_edge;
             if (dlt > 0.0) p.delta_min = dlt;
         }
+        if (const char *fx = getenv("PCH_DELTA_MAX")) {  // development: step cap
+            const double dlt = atof(fx) * m->mean_edge;
+            if (dlt > 0.0) p.delta_max = dlt;
+        }
+        p.delta0 = std::min(std::max(p.delta0, p.delta_min), p.delta_max);
         p.prof = getenv("PCH_PROFILE") ? 1 : 0;
         // chaining shortens the latency-bound single field; batched rows
         // are throughput bound and do better without it (fewer windows)

@@ -31,7 +31,7 @@ def parse(spec):
         k, v = kv.split("=")
         out[k] = float(v) if "." in v else int(v)
     env = {}
-    for key, var in (("dmin", "PCH_DELTA_MIN"), ("delta", "PCH_DELTA"), ("tpb", "PCH_TPB")):
+    for key, var in (("dmin", "PCH_DELTA_MIN"), ("delta", "PCH_DELTA"), ("dmax", "PCH_DELTA_MAX"), ("tpb", "PCH_TPB")):
         if key in out:
             env[var] = str(out.pop(key))
     out["_env"] = env
@@ -100,7 +100,7 @@ def main():
     for spec in specs:
         kw = parse(spec)
         env = kw.pop("_env")
-        for var in ("PCH_DELTA_MIN", "PCH_DELTA"):
+        for var in ("PCH_DELTA_MIN", "PCH_DELTA", "PCH_DELTA_MAX"):
             os.environ.pop(var, None)
         os.environ.update(env)
         cfg = EngineConfig(**kw)

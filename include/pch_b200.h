@@ -18,6 +18,8 @@
  *   pch_run_rows      batched single-source fields, one row per source
  *                     (the CLI's multi-source use, cli.py:382 context;
  *                      paper Table 3 "multiple-source-all-destination")
+ *   pch_fps           farthest-point sampling on seeded single-source solves
+ *                     (north star's batched workloads; no reference entry)
  * Error behaviour mirrors the reference: an empty or out-of-range source
  * list returns PCH_ERR_SOURCE (reference raises ValueError "invalid source
  * index"); exceeding max_iterations returns PCH_ERR_GUARD (EngineGuard,
@@ -132,6 +134,20 @@ int pch_run_device(pch_mesh *mesh, const int64_t *d_sources,
 int pch_run_rows(pch_mesh *mesh, const int64_t *sources, int64_t n_sources,
                  const pch_config *config, double *out_rows,
                  pch_stats *stats);
+
+/* Greedy farthest-point sampling (north star: batched multi-source
+ * workloads): sample 0 is `first`, sample s+1 the vertex with the largest
+ * geodesic distance to samples 0..s (ties: lowest index; +inf first, i.e.
+ * components not reached yet).  Each step is one solve seeded with the
+ * min-field so far, so it only propagates where the new sample is closer;
+ * the argmax stays on the device.  Writes int64 out_samples[n_samples]
+ * and, if out_dist is not NULL, the final min-field double[n_vertices]
+ * (= run_pch(mesh, out_samples) of the reference, engine.py:433).  No
+ * reference counterpart; the reference-side composition it replaces is a
+ * loop of run_pch calls with a host argmax. */
+int pch_fps(pch_mesh *mesh, int64_t first, int64_t n_samples,
+            const pch_config *config, int64_t *out_samples, double *out_dist,
+            pch_stats *stats);
 
 #ifdef __cplusplus
 }

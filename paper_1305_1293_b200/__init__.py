@@ -6,7 +6,8 @@ source indices in, per-vertex exact geodesic distances out, computed by a
 persistent sm_100a kernel behind the C ABI in ``include/pch_b200.h``.
 """
 from .engine import (DeviceMesh, EngineConfig, EngineGuard, RunStats,
-                     device_mesh, run_pch, run_pch_device, run_pch_rows)
+                     device_mesh, farthest_point_sampling, run_pch,
+                     run_pch_device, run_pch_rows)
 from .mesh import (BOUNDARY, MeshError, SurfaceMesh, VertexClass,
                    build_half_edge_mesh, classify_total_angle,
                    next_half_edge, prev_half_edge)
@@ -16,6 +17,7 @@ __version__ = "0.1.0"
 __all__ = [
     "BOUNDARY", "DeviceMesh", "EngineConfig", "EngineGuard", "MeshError",
     "RunStats", "SurfaceMesh", "VertexClass", "build_half_edge_mesh",
-    "classify_total_angle", "device_mesh", "next_half_edge",
+    "classify_total_angle", "device_mesh", "farthest_point_sampling",
+    "next_half_edge",
     "prev_half_edge", "run_pch", "run_pch_device", "run_pch_rows",
 ]

@@ -55,7 +55,7 @@ class PchStats(ctypes.Structure):
 # symbols declared in include/pch_b200.h
 EXPORTS = ("pch_abi_version", "pch_last_error", "pch_device_count",
            "pch_mesh_create", "pch_mesh_destroy", "pch_mesh_device_bytes",
-           "pch_run", "pch_run_device", "pch_run_rows")
+           "pch_run", "pch_run_device", "pch_run_rows", "pch_fps")
 
 _lib = None
 
@@ -90,6 +90,9 @@ def load():
     lib.pch_run_rows.argtypes = [P, P, i64, ctypes.POINTER(PchConfig), P,
                                  ctypes.POINTER(PchStats)]
     lib.pch_run_rows.restype = ctypes.c_int
+    lib.pch_fps.argtypes = [P, i64, i64, ctypes.POINTER(PchConfig), P, P,
+                            ctypes.POINTER(PchStats)]
+    lib.pch_fps.restype = ctypes.c_int
     if lib.pch_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libpch_b200.so ABI version mismatch")
     _lib = lib

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
@@ -117,6 +118,7 @@ struct Params {
     int rows;                  // distance fields solved together (batched rows)
     unsigned int *ccnt;        // live solver: per-CTA output counts [2 parity][S, P, fans][MAX_CTAS]
     int live_grid;             // CTAs of the live solver's launch (chunk count)
+    const double *seed;        // optional initial field (farthest-point sampling), else +inf
     unsigned long long *trace; // optional per-iteration timeline (TR_* records)
     long long trace_cap;       // iterations the trace buffer holds
 };
@@ -349,6 +351,8 @@ constexpr int TPB = PCH_TPB;      // threads per CTA of every solver kernel
 constexpr int NWARP = TPB / 32;
 constexpr double DELTA_FLOOR = 0.45;  // controller step floor, mean edge lengths
 constexpr double DELTA_CAP = 0.75;    // controller step cap, mean edge lengths
+constexpr double ALT_FLOOR = 1.0;     // ... and floor <= this many mean face altitudes
+constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
 constexpr int WIDE_ROWS = 8;          // from this many rows on, the 2-CTA/SM solver
@@ -1237,12 +1241,13 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
 // the proportional guess i * G / n and walks at most a few chunks.
 __device__ __forceinline__ unsigned long long chunk_slot(const unsigned int *pre, int G, unsigned int i,
                                                          unsigned long long ch) {
-    const unsigned int n = pre[G];
-    // fp32 guess: a 64-bit integer division is a long software sequence
-    int c = (int)((float)i * __frcp_rn((float)(n ? n : 1u)) * (float)G);
-    c = c < G - 1 ? c : G - 1;
-    while (c > 0 && pre[c] > i) --c;
-    while (c < G - 1 && pre[c + 1] <= i) ++c;
+    // the last chunk c with pre[c] <= i: branch-free binary search,
+    // log2(G) dependent shared loads whatever the chunk sizes' skew
+    int c = 0;
+    for (int step = 1 << (31 - __clz(G)); step > 0; step >>= 1) {
+        const int n = c + step;
+        c = (n < G && pre[n] <= i) ? n : c;
+    }
     return (unsigned long long)c * ch + (i - pre[c]);
 }
 
@@ -1422,7 +1427,15 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
         const unsigned int nwS = (nS + 31u) >> 5, nwP = (nP + 31u) >> 5;
         const unsigned int nwF = (nF + FANS_PER_WARP - 1u) / FANS_PER_WARP;
         const unsigned int W = nwS + nwF + nwP;
-        for (unsigned int wi = (unsigned int)gwid; wi < W; wi += (unsigned int)nwarps) {
+        // a batch item (up to `chain` propagations) costs several light
+        // items (fan candidate, pool re-examination): when the light items
+        // fit on the warps without a batch item at <= LIGHT_PER_WARP each,
+        // they stay there instead of wrapping onto the batch warps, whose
+        // chains set the iteration's latency
+        const unsigned int nLw = (unsigned int)nwarps > nwS ? (unsigned int)nwarps - nwS : 0u;
+        const bool split = nLw > 0u && nwF + nwP <= LIGHT_PER_WARP * nLw;
+        const unsigned int wstep = !split ? (unsigned int)nwarps : ((unsigned int)gwid < nwS ? W : nLw);
+        for (unsigned int wi = (unsigned int)gwid; wi < W; wi += wstep) {
             Win o0, o1, o2;   // o2: a sibling left behind by chaining
             int no = 0;
             bool h2 = false;
@@ -1610,13 +1623,17 @@ __global__ void k_init_state(Params p, const int64_t *src, int nsrc) {
     const long long n = (long long)gridDim.x * blockDim.x;
     const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     const long long nvr = (long long)p.nv * p.rows, nher = (long long)p.nhe * p.rows;
+    // a seed field (single field only) starts every vertex at a known
+    // path length: ICH pruning against it is as valid as against the
+    // solve's own distances, so the result is min(seed, new field)
+    const double *seed = p.rows == 1 ? p.seed : nullptr;
     for (long long v = t0; v < nvr; v += n) {
-        p.dist_new[v] = (unsigned long long)__double_as_longlong(INFINITY);
+        p.dist_new[v] = (unsigned long long)__double_as_longlong(seed ? seed[v] : INFINITY);
         p.fanpick[0][v] = make_ulonglong2(~0ull, ~0ull);
     }
     if (!p.live) {
         for (long long v = t0; v < p.nv; v += n) {
-            p.dist_cur[v] = INFINITY;
+            p.dist_cur[v] = seed ? seed[v] : INFINITY;
             p.fanpick[1][v] = make_ulonglong2(~0ull, ~0ull);
             p.fanpick[2][v] = make_ulonglong2(~0ull, ~0ull);
         }
@@ -1706,6 +1723,7 @@ struct pch_mesh {
     int device = 0;
     int32_t nv = 0, nhe = 0;
     double mean_edge = 1.0;
+    double mean_alt = 1.0;  // mean smallest altitude of a face (2 area / longest edge)
     FaceRec *face = nullptr;
     FanRec *fan = nullptr;
     FanHdr *fanhdr = nullptr;
@@ -1811,7 +1829,7 @@ static int ensure_ws(pch_mesh *m, long long cap, int rows) {
 // rows == nsrc > 1: one field per source, solved together (batched rows,
 // live solver only)
 static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *cfg,
-                 cudaStream_t st, pch_stats *stats, int rows = 1) {
+                 cudaStream_t st, pch_stats *stats, int rows = 1, const double *d_seed = nullptr) {
     if (cfg->k < 1) return fail(PCH_ERR_CONFIG, "k must be >= 1");
     if (!(cfg->epsilon_window > 0.0)) return fail(PCH_ERR_CONFIG, "epsilon_window must be > 0");
     if (cfg->fan_mode != 0 && cfg->fan_mode != 1) return fail(PCH_ERR_CONFIG, "fan_mode must be clip or full_edges");
@@ -1828,6 +1846,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         int rc = ensure_ws(m, cap, rows);
         if (rc) return rc;
         Params p = m->prm;
+        p.seed = d_seed;
         p.K = cfg->k;
         p.eps_win = cfg->epsilon_window;
         p.w0 = m->mean_edge / 64.0;
@@ -1844,7 +1863,9 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         // selecting several layers out of order; measured over the bench
         // meshes (profiles/r01_controller.md)
         p.delta0 = m->mean_edge;
-        p.delta_min = DELTA_FLOOR * m->mean_edge;
+        // skinny faces (torus-knot tubes): a step of several face
+        // altitudes selects layers out of order and doubles the windows
+        p.delta_min = std::min(DELTA_FLOOR * m->mean_edge, ALT_FLOOR * m->mean_alt);
         p.delta_max = DELTA_CAP * m->mean_edge;
         if (const char *fd = getenv("PCH_DELTA")) {  // development: fixed step
             const double dlt = atof(fd) * m->mean_edge;
@@ -1860,9 +1881,9 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         }
         p.delta0 = std::min(std::max(p.delta0, p.delta_min), p.delta_max);
         p.prof = getenv("PCH_PROFILE") ? 1 : 0;
-        // chaining shortens the latency-bound single field; batched rows
-        // are throughput bound and do better without it (fewer windows)
-        p.chain = cfg->chain > 0 ? cfg->chain : (rows >= WIDE_ROWS ? 1 : DEFAULT_CHAIN);
+        // chaining: two face crossings per iteration, for single fields
+        // and batched rows alike (profiles/r01_bigcheck.md)
+        p.chain = cfg->chain > 0 ? cfg->chain : DEFAULT_CHAIN;
         if (const char *ch = getenv("PCH_CHAIN")) p.chain = std::max(1, atoi(ch));  // development
         const char *trace_path = getenv("PCH_TRACE");
         if (trace_path && !m->trace) {
@@ -1969,6 +1990,73 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         }
         return PCH_OK;
     }
+}
+
+// ---------------------------------------------------------------------------
+// farthest-point sampling: argmax of the min-field, on the device
+
+// (distance, vertex) order of the greedy pick: larger distance first
+// (+inf = a component no sample reaches yet), then the lower vertex index
+__device__ __forceinline__ bool fps_better(double d, long long v, double bd, long long bv) {
+    return d > bd || (d == bd && v < bv);
+}
+
+__device__ __forceinline__ void fps_warp_best(double &bd, long long &bv) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double d = __shfl_down_sync(0xffffffffu, bd, o);
+        const long long v = __shfl_down_sync(0xffffffffu, bv, o);
+        if (fps_better(d, v, bd, bv)) {
+            bd = d;
+            bv = v;
+        }
+    }
+}
+
+// stage 1: one (distance, vertex) candidate per block
+__global__ void k_fps_argmax1(const double *field, long long nv, double *bd_out, long long *bv_out) {
+    __shared__ double sd[32];
+    __shared__ long long sv[32];
+    double bd = -1.0;
+    long long bv = LLONG_MAX;
+    for (long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+         v += (long long)gridDim.x * blockDim.x) {
+        const double d = __ldg(field + v);
+        if (fps_better(d, v, bd, bv)) {
+            bd = d;
+            bv = v;
+        }
+    }
+    fps_warp_best(bd, bv);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+        sd[w] = bd;
+        sv[w] = bv;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        bd = lane < nw ? sd[lane] : -1.0;
+        bv = lane < nw ? sv[lane] : LLONG_MAX;
+        fps_warp_best(bd, bv);
+        if (lane == 0) {
+            bd_out[blockIdx.x] = bd;
+            bv_out[blockIdx.x] = bv;
+        }
+    }
+}
+
+// stage 2: one warp reduces the block candidates into the next sample
+__global__ void k_fps_argmax2(const double *bd_in, const long long *bv_in, int nb, int64_t *next) {
+    double bd = -1.0;
+    long long bv = LLONG_MAX;
+    for (int i = threadIdx.x; i < nb; i += 32)
+        if (fps_better(bd_in[i], bv_in[i], bd, bv)) {
+            bd = bd_in[i];
+            bv = bv_in[i];
+        }
+    fps_warp_best(bd, bv);
+    if (threadIdx.x == 0) *next = (int64_t)bv;
 }
 
 // ---------------------------------------------------------------------------
@@ -2088,6 +2176,17 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
     m->nv = (int32_t)n_vertices;
     m->nhe = (int32_t)nhe;
     m->mean_edge = lsum / (double)nhe;
+    {
+        double asum = 0.0;
+        const int64_t nf = nhe / 3;
+        for (int64_t f = 0; f < nf; ++f) {
+            const double a = length[3 * f], b = length[3 * f + 1], c = length[3 * f + 2];
+            const double s = 0.5 * (a + b + c);
+            const double area = std::sqrt(std::max(0.0, s * (s - a) * (s - b) * (s - c)));
+            asum += 2.0 * area / std::max(std::max(a, b), std::max(c, 1e-300));
+        }
+        m->mean_alt = nf > 0 ? asum / (double)nf : m->mean_edge;
+    }
     auto cleanup = [&](int code, const std::string &msg) {
         pch_mesh_destroy(m);
         return fail(code, msg);
@@ -2209,6 +2308,54 @@ int pch_run_rows(pch_mesh *m, const int64_t *sources, int64_t n_sources, const p
     }
     CK(cudaStreamSynchronize(m->stream));
     return PCH_OK;
+}
+
+int pch_fps(pch_mesh *m, int64_t first, int64_t n_samples, const pch_config *cfg, int64_t *out_samples,
+            double *out_dist, pch_stats *stats) {
+    if (!m || !cfg || !out_samples) return fail(PCH_ERR_CONFIG, "null argument");
+    if (n_samples < 1) return fail(PCH_ERR_CONFIG, "n_samples must be >= 1");
+    int rc = check_sources(m, &first, 1);
+    if (rc) return rc;
+    CK(cudaSetDevice(m->device));
+    constexpr int NB = 4 * 148;  // argmax stage-1 blocks
+    const size_t need = sizeof(int64_t) * n_samples + sizeof(double) * m->nv +
+                        NB * (sizeof(double) + sizeof(long long));
+    // samples, the running min-field and the argmax scratch in one buffer
+    char *buf = nullptr;
+    CK(cudaMalloc(&buf, need));
+    int64_t *d_samples = reinterpret_cast<int64_t *>(buf);
+    double *d_min = reinterpret_cast<double *>(buf + sizeof(int64_t) * n_samples);
+    double *d_bd = d_min + m->nv;
+    long long *d_bv = reinterpret_cast<long long *>(d_bd + NB);
+    cudaStream_t st = m->stream;
+    auto done = [&](int code) {
+        cudaStreamSynchronize(st);
+        cudaFree(buf);
+        return code;
+    };
+    if (cudaMemcpyAsync(d_samples, &first, sizeof(int64_t), cudaMemcpyHostToDevice, st) != cudaSuccess)
+        return done(fail(PCH_ERR_CUDA, "sample upload failed"));
+    // greedy: sample s+1 is the vertex farthest from samples 0..s; each
+    // solve starts from the min-field so far and only moves where the new
+    // sample is closer (the argmax never leaves the device)
+    for (int64_t s = 0; s < n_samples; ++s) {
+        if ((rc = solve(m, d_samples + s, 1, cfg, st, stats, 1, s > 0 ? d_min : nullptr))) return done(rc);
+        if (cudaMemcpyAsync(d_min, field_ptr(m), sizeof(double) * m->nv, cudaMemcpyDeviceToDevice, st) !=
+            cudaSuccess)
+            return done(fail(PCH_ERR_CUDA, "field copy failed"));
+        if (s + 1 < n_samples) {
+            k_fps_argmax1<<<NB, 256, 0, st>>>(d_min, m->nv, d_bd, d_bv);
+            k_fps_argmax2<<<1, 32, 0, st>>>(d_bd, d_bv, NB, reinterpret_cast<int64_t *>(d_samples + s + 1));
+            if (cudaGetLastError() != cudaSuccess) return done(fail(PCH_ERR_CUDA, "argmax launch failed"));
+        }
+    }
+    if (cudaMemcpyAsync(out_samples, d_samples, sizeof(int64_t) * n_samples, cudaMemcpyDeviceToHost, st) !=
+            cudaSuccess ||
+        (out_dist &&
+         cudaMemcpyAsync(out_dist, d_min, sizeof(double) * m->nv, cudaMemcpyDeviceToHost, st) != cudaSuccess))
+        return done(fail(PCH_ERR_CUDA, "result download failed"));
+    if (cudaStreamSynchronize(st) != cudaSuccess) return done(fail(PCH_ERR_CUDA, "fps sync failed"));
+    return done(PCH_OK);
 }
 
 }  // extern "C"

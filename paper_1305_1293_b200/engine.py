@@ -253,6 +253,32 @@ def run_pch_rows(mesh: SurfaceMesh, sources, config: EngineConfig | None = None)
     return out, RunStats.from_native(st)
 
 
+def farthest_point_sampling(mesh: SurfaceMesh, n_samples: int, first: int = 0,
+                            config: EngineConfig | None = None):
+    """Greedy geodesic farthest-point sampling: sample 0 is ``first``,
+    sample s+1 the vertex farthest from samples 0..s (ties: lowest index;
+    unreached components first).  Returns ``(samples int64[n_samples],
+    min_field float64[n_vertices], RunStats)`` where ``min_field`` equals
+    ``run_pch(mesh, samples)[0]``.  One seeded solve per sample on the
+    device (include/pch_b200.h: pch_fps)."""
+    config = config or EngineConfig()
+    n = int(n_samples)
+    if n < 1:
+        raise ValueError("n_samples must be >= 1")
+    first = int(first)
+    if first < 0 or first >= mesh.n_vertices:
+        raise ValueError(f"invalid source index {first}")
+    dm = device_mesh(mesh, config.device)
+    samples = np.empty(n, dtype=np.int64)
+    out = np.empty(mesh.n_vertices, dtype=np.float64)
+    st = _native.PchStats()
+    cfg = config.to_native()
+    rc = dm._lib.pch_fps(dm.handle, first, n, ctypes.byref(cfg), samples.ctypes.data,
+                         out.ctypes.data, ctypes.byref(st))
+    _check(rc)
+    return samples, out, RunStats.from_native(st)
+
+
 def run_pch_device(mesh: SurfaceMesh, d_sources_ptr: int, n_sources: int,
                    d_out_ptr: int, config: EngineConfig | None = None,
                    stream: int = 0):

@@ -1,6 +1,6 @@
 """Parameter sweep of the GPU engine on a bench mesh (development tool).
 
-    python tools/sweep.py WORKLOAD "k=65536,chain=3;k=16384,dmin=0.4" [--trace]
+    python tools/sweep.py WORKLOAD "k=65536,chain=3;k=16384,dmin=0.4" [--trace] [--nocheck]
 
 (dmin / delta set the PCH_DELTA_MIN / PCH_DELTA development overrides:
 controller step floor / fixed step, in mean edge lengths.)
@@ -90,13 +90,19 @@ def main():
     m = M.bench_mesh(name)
     if name == "terrain1m":
         src = 354 * 709 + 354
+    elif name == "knot4m":
+        src = 0
     else:
         src = int(np.argmin(np.linalg.norm(m.positions - m.positions.mean(0), axis=1)))
     t = time.time()
-    ref, rs = O.run_ich(m, [src])
-    print(f"{name}: F={m.n_faces} src={src} ich={time.time() - t:.2f}s "
-          f"ich_windows={rs['total_windows_created']}", flush=True)
-    fin = np.isfinite(ref)
+    if "--nocheck" in sys.argv:
+        ref = None
+        print(f"{name}: F={m.n_faces} src={src} (no oracle check)", flush=True)
+    else:
+        ref, rs = O.run_ich(m, [src])
+        print(f"{name}: F={m.n_faces} src={src} ich={time.time() - t:.2f}s "
+              f"ich_windows={rs['total_windows_created']}", flush=True)
+        fin = np.isfinite(ref)
     for spec in specs:
         kw = parse(spec)
         env = kw.pop("_env")
@@ -113,8 +119,11 @@ def main():
             if best is None or st.time_kernel_ms < best[1].time_kernel_ms:
                 best = (d, st)
         d, st = best
-        same = np.array_equal(np.isfinite(d), fin)
-        err = float(np.max(np.abs(d[fin] - ref[fin]) / np.maximum(ref[fin], 1e-12))) if same else np.inf
+        if ref is None:
+            err = float("nan")
+        else:
+            same = np.array_equal(np.isfinite(d), fin)
+            err = float(np.max(np.abs(d[fin] - ref[fin]) / np.maximum(ref[fin], 1e-12))) if same else np.inf
         print(f"{spec:40s} kern={st.time_kernel_ms:8.2f}ms dev={st.time_device_ms:8.2f}ms "
               f"iters={st.iterations:6d} created={st.total_windows_created:10d} "
               f"prop={st.windows_propagated:10d} fans={st.fans_emitted:8d} "

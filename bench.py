@@ -240,7 +240,7 @@ def _rows_leg(args, ws, rank, local, dev):
     srcs = np.random.default_rng(4096).choice(mesh.n_vertices, total, replace=False)
     mine = srcs[shard_sources(srcs, rank, ws)]
     cfg = EngineConfig(device=local)
-    run_pch_rows(mesh, mine[:8], cfg)  # warm-up: upload, workspace
+    run_pch_rows(mesh, mine[:32], cfg)  # warm-up: upload, workspace of a full 32-row batch
     if ws > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -259,6 +259,35 @@ def _rows_leg(args, ws, rank, local, dev):
             "scaling": "weak", "batch_rows": 32,
             "windows_per_source": int(st.total_windows_created // max(len(mine), 1)),
             "timing": "wall clock, host sources in / host rows out, NCCL all-gather included"}
+
+
+def _fps_leg(args, ws, rank, local, dev, mesh):
+    """North star's second batched workload: greedy geodesic farthest-point
+    sampling (pch_fps) on the headline mesh.  Sequential by nature (sample
+    s+1 depends on samples 0..s), so N GPUs run N independent samplings
+    from different first vertices (weak scaling, no collective); wall time
+    of the whole job (max over ranks), host samples + min-field out."""
+    import torch
+    from paper_1305_1293_b200 import EngineConfig, farthest_point_sampling
+    cfg = EngineConfig(device=local)
+    first = int(np.random.default_rng(1234 + rank).integers(mesh.n_vertices))
+    farthest_point_sampling(mesh, 2, first, cfg)  # warm-up
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    samples, _, st = farthest_point_sampling(mesh, args.fps_samples, first, cfg)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t
+    tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+    dt = float(tt.item())
+    total = args.fps_samples * ws
+    return {"workload": args.workload, "samples": int(total), "samples_per_sec": round(total / dt, 2),
+            "seconds": round(dt, 3), "n_gpus": ws, "scaling": "weak",
+            "windows_propagated_per_sample": int(st.windows_propagated // args.fps_samples),
+            "timing": "wall clock, one seeded solve + device argmax per sample, host results"}
 
 
 def run_b200(args):
@@ -334,6 +363,7 @@ def run_b200(args):
     assert np.all(np.abs(host[fin] - field[fin]) <= 1e-9 * np.maximum(np.abs(field[fin]), 1e-12))
 
     rows_info = None if args.rows_per_rank <= 0 else _rows_leg(args, ws, rank, local, dev)
+    fps_info = None if args.fps_samples <= 0 else _fps_leg(args, ws, rank, local, dev, mesh)
 
     tot = torch.tensor([dev_ms, e2e_ms, kern_ms], dtype=torch.float64, device=dev)
     if ws > 1:
@@ -379,6 +409,8 @@ def run_b200(args):
         }
         if rows_info is not None:
             line["rows"] = rows_info
+        if fps_info is not None:
+            line["fps"] = fps_info
         if ws == 1 and not args.no_cpu_baseline:
             ref, ich, cb = _cpu_baseline(mesh, src)
             fin = np.isfinite(ref)
@@ -406,6 +438,8 @@ def main(argv=None):
     ap.add_argument("--ref-budget-s", type=float, default=150.0)
     ap.add_argument("--rows-per-rank", type=int, default=64,
                     help="configs[4] distance-matrix rows per GPU (0 = skip)")
+    ap.add_argument("--fps-samples", type=int, default=32,
+                    help="farthest-point samples per GPU on the headline mesh (0 = skip)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

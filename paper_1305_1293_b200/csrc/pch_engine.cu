@@ -125,7 +125,7 @@ struct Params {
 
 // per-iteration trace record (PCH_TRACE=path): globaltimer stamps and sizes
 enum { TR_T0, TR_A_END, TR_B1, TR_B_END, TR_B2, TR_NS, TR_NP, TR_NC, TR_NF, TR_NTV, TR_TSEL_BITS,
-       TR_FAN_END, TR_START_MAX, TR_WORK_END, TR_SCAN_END, TR_TRIP0, TR_LOADED, TR_N };
+       TR_FAN_END, TR_START_MAX, TR_WORK_END, TR_SCAN_END, TR_TRIP0, TR_LOADED, TR_ROUTED, TR_N };
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -352,6 +352,7 @@ constexpr int NWARP = TPB / 32;
 constexpr double DELTA_FLOOR = 0.45;  // controller step floor, mean edge lengths
 constexpr double DELTA_CAP = 0.75;    // controller step cap, mean edge lengths
 constexpr double ALT_FLOOR = 1.0;     // ... and floor <= this many mean face altitudes
+constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more crossing
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
@@ -1561,6 +1562,7 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
             if (no > 1) put_at(s1, s1 ? sa++ : pa++, o1);
             if (h2) put_at(s2, s2 ? sa : pa, o2);
             ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
+            if (p.trace && wi < nwS) trace_max_warp(p, it, TR_ROUTED);
             pend.complete();
             if (p.trace && wi < nwS) trace_max_warp(p, it, TR_SCAN_END);
             if (++iters_since_fold == FOLD_TRIPS) {
@@ -1862,11 +1864,20 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         // keeps narrow ones (terrain: fewer than k windows per layer) from
         // selecting several layers out of order; measured over the bench
         // meshes (profiles/r01_controller.md)
+        // chaining: up to `chain` face crossings per iteration, for single
+        // fields and batched rows alike; a third crossing pays on large
+        // meshes (deep wavefronts), not on small ones where it only
+        // lengthens the iteration (profiles/r01_controller.md)
+        p.chain = cfg->chain > 0 ? cfg->chain
+                                 : (m->nhe / 3 >= LONG_CHAIN_FACES ? DEFAULT_CHAIN + 1 : DEFAULT_CHAIN);
+        if (const char *ch = getenv("PCH_CHAIN")) p.chain = std::max(1, atoi(ch));  // development
         p.delta0 = m->mean_edge;
         // skinny faces (torus-knot tubes): a step of several face
-        // altitudes selects layers out of order and doubles the windows
-        p.delta_min = std::min(DELTA_FLOOR * m->mean_edge, ALT_FLOOR * m->mean_alt);
-        p.delta_max = DELTA_CAP * m->mean_edge;
+        // altitudes selects layers out of order and doubles the windows.
+        // The bounds are per two crossings and scale with the chain length.
+        const double per_cross = 0.5 * p.chain;
+        p.delta_min = per_cross * std::min(DELTA_FLOOR * m->mean_edge, ALT_FLOOR * m->mean_alt);
+        p.delta_max = per_cross * DELTA_CAP * m->mean_edge;
         if (const char *fd = getenv("PCH_DELTA")) {  // development: fixed step
             const double dlt = atof(fd) * m->mean_edge;
             if (dlt > 0.0) p.delta0 = p.delta_min = p.delta_max = dlt;
@@ -1881,10 +1892,6 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         }
         p.delta0 = std::min(std::max(p.delta0, p.delta_min), p.delta_max);
         p.prof = getenv("PCH_PROFILE") ? 1 : 0;
-        // chaining: two face crossings per iteration, for single fields
-        // and batched rows alike (profiles/r01_bigcheck.md)
-        p.chain = cfg->chain > 0 ? cfg->chain : DEFAULT_CHAIN;
-        if (const char *ch = getenv("PCH_CHAIN")) p.chain = std::max(1, atoi(ch));  // development
         const char *trace_path = getenv("PCH_TRACE");
         if (trace_path && !m->trace) {
             m->trace_cap = 1 << 17;

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 TR = ("t0", "a_end", "b1", "b_end", "b2", "ns", "np", "nc", "nf", "ntv", "tsel", "fan_end",
-      "start_max", "work_end", "scan_end", "trip0", "loaded")
+      "start_max", "work_end", "scan_end", "trip0", "loaded", "routed")
 
 
 def parse(spec):
@@ -72,6 +72,11 @@ def trace_summary(path):
               f"scan(->max scan end)={np.mean(se[ok] - we[ok])/1e3:.2f}us "
               f"rest(->A end)={np.mean(ae[ok] - se[ok])/1e3:.2f}us", flush=True)
         t0m, ld = a[:, 15], a[:, 16]
+        rt = a[:, 17]
+        ok3 = ok & (rt > 0)
+        if ok3.any():
+            print(f"   routed(before fan-pick completion, max)={np.mean(rt[ok3] - t0[ok3])/1e3:.2f}us "
+                  f"scan end(after)={np.mean(se[ok3] - t0[ok3])/1e3:.2f}us", flush=True)
         ok2 = ok & (t0m > 0) & (ld > 0)
         if ok2.any():
             print(f"   setup(t0->max trip0)={np.mean(t0m[ok2] - t0[ok2])/1e3:.2f}us "

@@ -1321,7 +1321,13 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
     double t = 0.0;           // threshold S_i was selected with
     double delta = p.delta0;  // controller step
     // prefix tables of the iteration's inputs from the per-CTA counts
-    auto build_prefix = [&](int par_in, int par_fan) {
+    // (and, with `slot`, the controller's inputs in the same round trip)
+    auto build_prefix = [&](int par_in, int par_fan, const Slot *slot) {
+        if (slot && threadIdx.x == 96) {
+            s_c[0] = (unsigned long long)__ldcg(&ctrl->error);
+            s_c[1] = __ldcg(&slot->pmin);
+            s_c[2] = __ldcg(&slot->smax);
+        }
         if (threadIdx.x < 96) {
             const int q = threadIdx.x >> 5;  // 0: S, 1: P, 2: fans of the previous iteration
             const unsigned int *cnt = p.ccnt + (size_t)((q < 2 ? par_in : par_fan) * 3 + q) * MAX_CTAS;
@@ -1353,13 +1359,7 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
         }
         __syncthreads();
     };
-    build_prefix(0, 1);  // S_0: the source windows (chunk-published by k_source_windows)
-    if (threadIdx.x == 0) {
-        s_c[0] = 0ull;
-        s_c[1] = *(volatile unsigned long long *)&ctrl->slot[0].pmin;
-        s_c[2] = *(volatile unsigned long long *)&ctrl->slot[0].smax;
-    }
-    __syncthreads();
+    build_prefix(0, 1, &ctrl->slot[0]);  // S_0: the source windows (chunk-published by k_source_windows)
     int it = 0;
     for (;;) {
         const int par = it & 1;                     // parity of the iteration's inputs
@@ -1589,14 +1589,11 @@ __global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
                 if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
             }
         }
-        grid_barrier(ctrl, gen, [&] {
-            s_c[0] = (unsigned long long)*(volatile int *)&ctrl->error;
-            s_c[1] = *(volatile unsigned long long *)&nxt.pmin;
-            s_c[2] = *(volatile unsigned long long *)&nxt.smax;
-        });
+        grid_barrier(ctrl, gen);
         // the next iteration's inputs: S_{i+1}, P_{i+1} (parity par^1) and
-        // the fan candidates of iteration i (parity par)
-        build_prefix(par ^ 1, par);
+        // the fan candidates of iteration i (parity par); the counts and
+        // the controller's inputs are read in one round trip
+        build_prefix(par ^ 1, par, &nxt);
         const int err = (int)s_c[0];
         const unsigned int ns = s_pre[0][G], np = s_pre[1][G], nf = s_pre[2][G];
         if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {

@@ -356,7 +356,6 @@ constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more c
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
-constexpr int WIDE_ROWS = 8;          // from this many rows on, the 2-CTA/SM solver
 constexpr int MAX_CTAS = 1024;        // chunk-count tables of the live solver
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
@@ -1232,10 +1231,6 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
 //     only weakens pruning).  Fields agree across runs to rounding; the
 //     bitwise-deterministic two-barrier kernel above is PCH_FLAG_DETERMINISTIC.
 
-// MINB = resident CTAs per SM the register budget targets: 1 for single
-// fields (latency bound: the propagation chain, 216 registers, no spills),
-// 2 for batched rows (throughput bound: twice the warps per SM hide the
-// chain's latency, at the price of a few register spills)
 // Item index -> slot of a chunked buffer: chunk c holds items
 // [pre[c], pre[c+1]) at slots c * ch + (i - pre[c]).  Chunks are filled
 // about evenly (windows are spread over the CTAs), so the search starts at
@@ -1276,12 +1271,11 @@ __device__ __forceinline__ void warp_chunk_alloc2(unsigned long long *s_cnt, uns
     pa = (unsigned int)(base >> 32) + (ex >> 16);
 }
 
-// MINB = resident CTAs per SM the register budget targets: 1 for single
-// fields (latency bound: the propagation chain, no spills), 2 for batched
-// rows (throughput bound: twice the warps per SM hide the chain's latency,
-// at the price of some register spills)
-template <int MINB>
-__global__ void __launch_bounds__(TPB, MINB) pch_live(Params p) {
+// One CTA per SM with the full register budget (no spills), for single
+// fields and batched rows alike: a 2-CTA/SM build at 128 registers spilled
+// the propagation state to local memory and lost 9-16 % on batched rows
+// (profiles/r01_bigcheck.md)
+__global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
     // Outputs are chunked per CTA: CTA b writes the windows it routes to
     // slots [b*ch, (b+1)*ch) of the next batch / pool and its fan
     // candidates to [b*chF, (b+1)*chF), allocating with one shared atomic
@@ -1738,7 +1732,7 @@ struct pch_mesh {
     double *d_out = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
-    int grid = 0, grid_live = 0, grid_live2 = 0;
+    int grid = 0, grid_live = 0;
     unsigned long long *trace = nullptr;  // PCH_TRACE development timeline
     long long trace_cap = 0;
 };
@@ -1899,8 +1893,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         if (p.trace) CK(cudaMemsetAsync(p.trace, 0, sizeof(unsigned long long) * TR_N * p.trace_cap, st));
         CK(cudaEventRecord(m->ev0, st));
         CK(cudaMemsetAsync(p.ctrl, 0, sizeof(Ctrl), st));
-        const bool wide = rows >= WIDE_ROWS && m->grid_live2 > 0;
-        p.live_grid = wide ? m->grid_live2 : m->grid_live;
+        p.live_grid = m->grid_live;
         if (p.live) CK(cudaMemsetAsync(p.ccnt, 0, sizeof(unsigned int) * 2 * 3 * MAX_CTAS, st));
         k_init_state<<<4 * 148, 256, 0, st>>>(p, d_src, nsrc);
         CK(cudaGetLastError());
@@ -1912,7 +1905,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         void *args[] = {&p};
         if (p.live)
         {
-            const void *kern = wide ? (const void *)pch_live<2> : (const void *)pch_live<1>;
+            const void *kern = (const void *)pch_live;
             CK(cudaLaunchCooperativeKernel(kern, dim3(p.live_grid), dim3(TPB), args, 0, st));
         }
         else
@@ -2215,14 +2208,11 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
     int nsm = 0, per_sm = 0, per_sm_live = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_persistent, TPB, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live<1>, TPB, 0);
-    int per_sm_live2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live2, pch_live<2>, TPB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live, TPB, 0);
     if (per_sm < 1 || per_sm_live < 1) return cleanup(PCH_ERR_CUDA, "persistent kernel cannot be resident");
     // persistent grids: every SM, as many co-resident CTAs as fit (<= 4)
     m->grid = nsm * std::min(per_sm, 4);
     m->grid_live = nsm * std::min(per_sm_live, 4);
-    m->grid_live2 = per_sm_live2 >= 2 ? nsm * std::min(per_sm_live2, 4) : 0;
     *out = m;
     return PCH_OK;
 }

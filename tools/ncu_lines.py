@@ -46,7 +46,7 @@ def main():
     lib = sys.argv[3] if len(sys.argv) > 3 else os.path.join(
         ROOT, "paper_1305_1293_b200", "_lib", "libpch_b200.so")
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-    # the report names kernels demangled (pch_live<1>), the cubin mangled
+    # the report names kernels demangled (pch_live), the cubin mangled
     # (_Z8pch_liveILi1EEv6Params): filter the report on the plain name
     ncu_name = re.sub(r"ILi\d+.*", "", kernel)
     txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv",

@@ -48,9 +48,8 @@ enum { ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_PRUNE_TINY,
        ST_PRUNE_DEGEN, ST_RECHECK, ST_STORED, ST_EV_CREATED, ST_EV_APPLIED,
        ST_FANS, ST_MAXCHILD, ST_PEAK,
        // PCH_PROFILE section clocks (clock64 deltas summed over threads)
-       ST_CYC_LOAD, ST_CYC_PROP, ST_CYC_EVENTS, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
-       ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CYC_P1, ST_CYC_P2, ST_CYC_P3, ST_CYC_P4,
-       ST_CYC_P5, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES, N_ST };
+       ST_CYC_PROP, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
+       ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES, N_ST };
 
 enum { ERR_NONE = 0, ERR_OVERFLOW = 1, ERR_GUARD = 2, ERR_TIMEOUT = 3 };
 
@@ -1938,20 +1937,12 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
                 if (c.lat_hist[b]) fprintf(stderr, " [2^%d]=%llu", b, c.lat_hist[b]);
             fprintf(stderr, "\n");
             const unsigned long long *q = c.st;
-            fprintf(stderr, "PCH_PROFILE prop sections cycles/propagation: window %.0f face+split %.0f "
-                    "dist %.0f unfold+recheck %.0f children %.0f events %.0f\n",
-                    q[ST_CYC_P1] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
-                    q[ST_CYC_P2] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
-                    q[ST_CYC_P3] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
-                    q[ST_CYC_P4] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
-                    q[ST_CYC_P5] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1),
-                    q[ST_CYC_EVENTS] / (double)std::max<unsigned long long>(q[ST_PROPAGATED], 1));
             double np_ = (double)std::max<unsigned long long>(q[ST_PROPAGATED] + q[ST_RECHECK], 1);
             fprintf(stderr,
-                    "PCH_PROFILE cycles/unit: load %.0f prop %.0f (events %.0f) pool %.0f "
+                    "PCH_PROFILE cycles/unit: prop %.0f pool %.0f "
                     "fanspan %.0f/fan fanitem %.0f part %.0f | n_prop %.0f n_pool %llu n_fanitem %llu "
                     "n_part %llu\n",
-                    q[ST_CYC_LOAD] / np_, q[ST_CYC_PROP] / np_, q[ST_CYC_EVENTS] / np_,
+                    q[ST_CYC_PROP] / np_,
                     q[ST_CYC_POOL] / (double)std::max<unsigned long long>(q[ST_N_POOL], 1),
                     q[ST_CYC_FANSPAN] / (double)std::max<unsigned long long>(q[ST_FANS], 1),
                     q[ST_CYC_FANITEM] / (double)std::max<unsigned long long>(q[ST_N_FANITEM], 1),

@@ -40,7 +40,7 @@ def main():
             src = 0
         rec = {"faces": int(m.n_faces), "vertices": int(m.n_vertices), "build_s": round(tb, 1),
                "source": src}
-        for k in (16384, 65536):
+        for k in (65536, 16384):  # the default (16384) last: its field is checked
             best = None
             for _ in range(3):
                 d, st = run_pch(m, [src], EngineConfig(k=k))
@@ -58,6 +58,11 @@ def main():
         rec["ich_windows"] = rs["total_windows_created"]
         rec["max_rel_err"] = rel(d, ref)
         rec["unreachable"] = int(np.sum(~np.isfinite(d)))
+        rec["unreachable_ich"] = int(np.sum(~np.isfinite(ref)))
+        both = np.isfinite(d) & np.isfinite(ref)
+        rec["unreachable_both"] = int(np.sum(~np.isfinite(d) & ~np.isfinite(ref)))
+        rec["max_rel_err_shared"] = float(np.max(np.abs(d[both] - ref[both]) /
+                                                 np.maximum(np.abs(ref[both]), 1e-12)))
         print(name, "ich", rec["ich_s"], "s err", rec["max_rel_err"], flush=True)
         if name == "torus500k":
             rng = np.random.default_rng(4096)

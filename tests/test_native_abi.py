@@ -95,3 +95,24 @@ def test_no_device_raises_loudly():
     from paper_1305_1293_b200 import run_pch
     with pytest.raises(_native.NativeUnavailable):
         run_pch(meshes.make("cube"), [0])
+
+
+def test_fps_argument_validation(cube):
+    """farthest_point_sampling rejects bad arguments before touching the
+    device (the same ValueError contract as run_pch's sources)."""
+    from paper_1305_1293_b200 import farthest_point_sampling
+    with pytest.raises(ValueError):
+        farthest_point_sampling(cube, 0, 0)
+    with pytest.raises(ValueError, match="invalid source index"):
+        farthest_point_sampling(cube, 2, cube.n_vertices)
+    with pytest.raises(ValueError):
+        farthest_point_sampling(cube, 2, -1)
+
+
+def test_fps_no_device_raises_loudly(cube):
+    lib = _native.load()
+    if lib.pch_device_count() > 0:
+        pytest.skip("a CUDA device is present")
+    from paper_1305_1293_b200 import farthest_point_sampling
+    with pytest.raises(_native.NativeUnavailable):
+        farthest_point_sampling(cube, 2, 0)

@@ -47,8 +47,9 @@ def main():
         ROOT, "paper_1305_1293_b200", "_lib", "libpch_b200.so")
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
     # the report names kernels demangled (pch_live), the cubin mangled
-    # (_Z8pch_liveILi1EEv6Params): filter the report on the plain name
-    ncu_name = re.sub(r"ILi\d+.*", "", kernel)
+    # (_Z8pch_live6Params): filter the report on the plain name
+    m = re.match(r"_Z(\d+)", kernel)
+    ncu_name = kernel[len(m.group(0)):len(m.group(0)) + int(m.group(1))] if m else kernel
     txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv",
                           "-k", f"regex:{ncu_name}"],
                          capture_output=True, text=True).stdout

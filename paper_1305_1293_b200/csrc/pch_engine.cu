@@ -223,18 +223,24 @@ __device__ __forceinline__ double gdist(const Params &p, const RowTabs &t, int32
     if (p.live) return __longlong_as_double((long long)__ldcg(t.dist + v));
     return __ldcg(p.dist_cur + v);
 }
-__device__ __forceinline__ double2 gsplit(const Params &p, const RowTabs &t, int32_t j, ulonglong2 &raw) {
+// the angle-split entry as ord64 bits (the CAS guess), converted where it
+// is used: keeping the conversion away from the load lets the load's
+// latency overlap the unfolding and both children's geometry
+__device__ __forceinline__ ulonglong2 gsplit_raw(const Params &p, const RowTabs &t, int32_t j) {
     if (p.live) {
-        // 128-bit atomic read (the compare value never matches: ord64 of a
-        // comparison distance always has its top bit set)
-        raw = atomicCAS(t.split + j, make_ulonglong2(0ull, 0ull), make_ulonglong2(0ull, 0ull));
-        return make_double2(unord64(raw.x), unord64(raw.y));
+        // single-copy-atomic 128-bit read (a strong .b128 load): the pair is
+        // never torn between two claims' CAS writes
+        unsigned long long lo, hi;
+        asm volatile("{\n\t.reg .b128 t;\n\tld.relaxed.gpu.global.b128 t, [%2];\n\tmov.b128 {%0, %1}, t;\n\t}"
+                     : "=l"(lo), "=l"(hi)
+                     : "l"(t.split + j)
+                     : "memory");
+        return make_ulonglong2(lo, hi);
     }
-    double2 s = __ldcg(p.split_cur + j);
     // the frozen entry is the shadow entry's value at the start of the
     // iteration: the best first guess for a CAS on it
-    raw = make_ulonglong2(ord64(s.x), ord64(s.y));
-    return s;
+    const double2 s = __ldcg(p.split_cur + j);
+    return make_ulonglong2(ord64(s.x), ord64(s.y));
 }
 
 __device__ __forceinline__ int key_bin(double key, double base, double w) {
@@ -714,8 +720,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const uint32_t v0f = w.v0f, v1f = w.v1f, vdf = far ? w.vdf : 0u;
     const int32_t cho_l = __ldg(&fp->opp[a1]), cho_r = __ldg(&fp->opp[a2]);
     const uint32_t apx_l = __ldg(&fp->apx[a1]), apx_r = __ldg(&fp->apx[a2]);
-    ulonglong2 sp_raw = make_ulonglong2(0ull, 0ull);
-    const double2 sp = far ? gsplit(p, T, j, sp_raw) : make_double2(INFINITY, 0.0);
+    const ulonglong2 sp_raw = far ? gsplit_raw(p, T, j) : make_ulonglong2(ord64(INFINITY), ord64(0.0));
     // level 2: distances at the three vertices
     const int32_t v0 = (int32_t)(v0f & VMASK), v1 = (int32_t)(v1f & VMASK);
     const int32_t vd = (int32_t)(vdf & VMASK);
@@ -733,24 +738,19 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
         ls.add(ST_PRUNE_DEGEN);
         return 0;
     }
-    if (p.recheck) {
-        // endpoint inequalities of the ICH filter (paper Fig. 4b) against
-        // the current field: paths through v0 (resp. v1) already reach the
-        // far end of the interval more cheaply -> the window is useless
-        // |I B| = d1 and |I A| = d0 by construction of I
-        const double tB = dps + d1, tA = dps + d0;
-        if ((tB > g0 + b1 + EPS_NUM) || (tA > g1 + (ell - b0) + EPS_NUM)) {
-            ls.add(ST_RECHECK);
-            return 0;
-        }
-    }
-    ls.add(ST_PROPAGATED);
+    // endpoint inequalities of the ICH filter (paper Fig. 4b) against the
+    // current field: paths through v0 (resp. v1) already reach the far end
+    // of the interval more cheaply -> the window is useless.  Evaluated
+    // here, applied at the end (no branch on the distance loads).
+    // |I B| = d1 and |I A| = d0 by construction of I
+    const bool rechecked = p.recheck && ((dps + d1 > g0 + b1 + EPS_NUM) ||
+                                         (dps + d0 > g1 + (ell - b0) + EPS_NUM));
 
     // interval endpoints sitting on v0 / v1 (geom.py:345-385)
     const double cand0 = dps + d0 + b0;
-    const bool ev0 = b0 <= p.eps_win && cand0 < g0;
+    const bool ev0 = !rechecked && b0 <= p.eps_win && cand0 < g0;
     const double cand1 = dps + d1 + (ell - b1);
-    const bool ev1 = b1 >= ell - p.eps_win && cand1 < g1;
+    const bool ev1 = !rechecked && b1 >= ell - p.eps_win && cand1 < g1;
 
     // the far triangle: apex D below the edge (geom.py:387-516)
     const double dx = 0.5 * (ell * ell + lan * lan - lpv * lpv) / ell;
@@ -773,12 +773,6 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const double comp = dps + nvd;
     const double denom = iy - dy;
     const double entry_x = denom > 1e-300 ? ix + (dx - ix) * (iy / denom) : ix;
-    // one-angle-one-split (Fig. 4a): a stored window that already gives
-    // the apex a shorter distance leaves only the child on our side
-    const bool claim = occ && comp < sp.x;
-    const bool split_pruned = occ && !claim;
-    const bool want_l = occ ? (claim || entry_x < sp.y) : (far && left);
-    const bool want_r = occ ? (claim || !(entry_x < sp.y)) : (far && !left);
     // the two rays: I->A against the left edge (v0, D) unless only the
     // right edge is hit, I->B against the right edge (D, v1) unless only
     // the left edge is hit
@@ -790,7 +784,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
                              eB_left ? dx : ell, eB_left ? dy : 0.0, rB);
     const bool okL = okA && (occ || okB), okR = okB && (occ || okA);
     const double candd = comp;
-    const bool evd = occ && candd < gdd;
+    const bool evd = !rechecked && occ && candd < gdd;
     int nc = 0;
     Win cl, cr;
     const int fl = make_child(3 * (fr / 3) + a1, cho_l, v0f, vdf, apx_l, lan, 0.0, 0.0, dx, dy, rA,
@@ -800,13 +794,25 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
                                occ ? 0.0 : rA, rB,
                                ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, cr);
     cl.row = cr.row = w.row;
+    // one-angle-one-split (Fig. 4a): a stored window that already gives
+    // the apex a shorter distance leaves only the child on our side
+    const double sp_comp = unord64(sp_raw.x), sp_x = unord64(sp_raw.y);
+    const bool claim = !rechecked && occ && comp < sp_comp;
+    const bool split_pruned = !rechecked && occ && !claim;
+    const bool want_l = !rechecked && (occ ? (claim || entry_x < sp_x) : (far && left));
+    const bool want_r = !rechecked && (occ ? (claim || !(entry_x < sp_x)) : (far && !left));
     const bool ml = want_l && okL, mr = want_r && okR;  // children computed
     const bool sl = ml && fl == CH_STORED, sr = mr && frr == CH_STORED;
     // accounting as the reference counts it (geom.py:433-516)
+    ls.add(ST_PROPAGATED, rechecked ? 0u : 1u);
+    ls.add(ST_RECHECK, rechecked ? 1u : 0u);
     ls.add(ST_PRUNE_SPLIT, split_pruned ? 1 : 0);
-    ls.add(ST_CREATED, (split_pruned ? 1 : 0) + (occ ? (want_l ? 1 : 0) + (want_r ? 1 : 0) : (far ? 1 : 0)));
-    const unsigned int degen = occ ? (want_l && !okL ? 1u : 0u) + (want_r && !okR ? 1u : 0u)
-                                   : (far && !(okA && okB) ? 1u : 0u);
+    ls.add(ST_CREATED, rechecked ? 0u
+                                 : (split_pruned ? 1u : 0u) +
+                                       (occ ? (want_l ? 1u : 0u) + (want_r ? 1u : 0u) : (far ? 1u : 0u)));
+    const unsigned int degen = rechecked ? 0u
+                               : occ     ? (want_l && !okL ? 1u : 0u) + (want_r && !okR ? 1u : 0u)
+                                         : (far && !(okA && okB) ? 1u : 0u);
     ls.add(ST_PRUNE_DEGEN, degen + (ml && fl == CH_DEGEN ? 1u : 0u) + (mr && frr == CH_DEGEN ? 1u : 0u));
     ls.add(ST_PRUNE_TINY, (ml && fl == CH_TINY ? 1u : 0u) + (mr && frr == CH_TINY ? 1u : 0u));
     ls.add(ST_PRUNE_ICH, (ml && fl == CH_ICH ? 1u : 0u) + (mr && frr == CH_ICH ? 1u : 0u));

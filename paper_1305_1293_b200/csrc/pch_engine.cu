@@ -7,13 +7,16 @@
 // (pch_device.cuh, reference geom.py) and the event primitives:
 //
 //   pch_live (default)   one phase + one grid barrier per iteration: the
-//            next threshold is fixed up front by a step controller, every
-//            produced window is routed to the next batch or the pool as it
-//            is produced (CTA-wide scan, one reservation per CTA), the
-//            filters read the tables the events update atomically, and a
-//            child inside the next threshold is propagated at once by the
-//            same thread (chaining).  Also solves R fields at once
-//            (batched rows, pch_run_rows).
+//            next threshold is fixed up front by a step controller (about
+//            one face layer per crossing), every produced window is routed
+//            to the next batch or the pool as it is produced (into the
+//            CTA's own chunk, one shared atomic per warp; chunk prefix
+//            tables rebuilt after the barrier), the filters read the tables
+//            the events update atomically, and a child inside the next
+//            threshold is propagated at once by the same thread (chaining,
+//            up to 3 crossings per iteration).  Also solves R fields at
+//            once (batched rows, pch_run_rows) and seeded fields
+//            (farthest-point sampling, pch_fps).
 //   pch_persistent (PCH_FLAG_DETERMINISTIC)   two phases per iteration:
 //            propagation against tables frozen at the start of the
 //            iteration, then commit + histogram k-selection + partition

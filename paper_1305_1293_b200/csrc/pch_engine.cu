@@ -420,25 +420,9 @@ __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, S
     }
 }
 
-// A fan-pick claim whose first CAS attempt is in flight: the live solver
-// issues it during the propagation and completes it (retrying if the pick
-// moved) after the window's children are routed, so the round trip
-// overlaps that work.  One per thread; further claims are synchronous.
-struct FanPend {
-    ulonglong2 *ptr;
-    ulonglong2 guess, want, seen;
-    bool active;
-    bool enabled;
-    __device__ __forceinline__ void complete() {
-        if (!active) return;
-        active = false;
-        if (seen.x != guess.x || seen.y != guess.y) cas_min_u128(ptr, want.x, want.y, seen);
-    }
-};
-
 template <typename FanSink>
 __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uint32_t row, FanSink &&sink,
-                                          FanPend &pend, ulonglong2 guess, int32_t v, int32_t anchor,
+                                          ulonglong2 guess, int32_t v, int32_t anchor,
                                           double cand, double ax, double ay, double bx, double by) {
     FanEv e;
     e.v = v;
@@ -456,17 +440,15 @@ __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uin
     // same fan (the reference dedupes those rows, engine.py:201).  The
     // deterministic solver resets the picks every iteration; the live one
     // never does (a new candidate is always strictly smaller) and seeds the
-    // CAS with the pick it read, so a claim is one round trip.
+    // CAS with the pick it read.
     const unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
     const unsigned long long lo = fan_tiebreak(e);
-    if (pend.enabled && !pend.active) {
-        if (hi < guess.x || (hi == guess.x && lo < guess.y)) {
-            pend.ptr = t.pick + v;
-            pend.guess = guess;
-            pend.want = make_ulonglong2(hi, lo);
-            pend.seen = atomicCAS(pend.ptr, guess, pend.want);
-            pend.active = true;
-        }
+    if (p.live) {
+        // one attempt, reply unused (no wait on the propagation path): if
+        // it loses a race against a worse candidate, the winner check of
+        // the next iteration finds the pick stale and repairs it
+        if (hi < guess.x || (hi == guess.x && lo < guess.y))
+            atomicCAS(t.pick + v, guess, make_ulonglong2(hi, lo));
     } else {
         int tries = 0;
         cas_min_u128(t.pick + v, hi, lo, guess, &tries);
@@ -691,7 +673,7 @@ __device__ void emit_fan(const Params &p, const RowTabs &t, uint32_t row, int32_
 // Up to two children are returned in `c`; events go to the shadow tables.
 
 template <typename FanSink>
-__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, FanSink &&fsink, FanPend &pend,
+__device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, FanSink &&fsink,
                                          const Win &w, Win &out0, Win &out1, LocalStats &ls) {
     // Latency layout: the per-iteration critical path is one propagation
     // (of the slowest lane of the slowest warp), so
@@ -836,13 +818,13 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     if (claim) angle_event(p, T, sg, j, comp, entry_x, sp_raw, ls);
     // saddle fans (Fig. 3c): the reverse direction of the incoming ray
     // relative to an anchor half-edge out of the vertex (geom.py:353-484)
-    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, fsink, pend, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
+    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, fsink, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
     if (ev1 && (v1f & SADDLE_BIT)) {
         if (far) {
             // anchor jo = v1 -> v0: its wedge follows next(j)'s, so this is
             // the reference's anchor next(j) with the corner at v1 folded
             // into the anchor angle
-            fan_event(p, T, w.row, fsink, pend, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
+            fan_event(p, T, w.row, fsink, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
         } else {
             // boundary window: anchor next(j), the source-side apex
             // direction from v1 (geom.py:372-377)
@@ -853,12 +835,12 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
             const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
             const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
             const double ay2 = lps * lps - axs * axs;
-            fan_event(p, T, w.row, fsink, pend, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
+            fan_event(p, T, w.row, fsink, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
                       ay2 > 0.0 ? sqrt(ay2) : 0.0);
         }
     }
     if (evd && (vdf & SADDLE_BIT))
-        fan_event(p, T, w.row, fsink, pend, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
+        fan_event(p, T, w.row, fsink, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
     return nc;
 }
 
@@ -1050,9 +1032,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 if (i < nS) {
                     long long c0 = p.prof ? clock64() : 0;
                     Win win = load_win(p.S, i);
-                    FanPend sync_pend{};
-                    sync_pend.enabled = false;
-                    nc = propagate(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, sync_pend, win, ca,
+                    nc = propagate(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, win, ca,
                                    cb, ls);
                     if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
                     if (nc > maxchild) maxchild = nc;
@@ -1442,8 +1422,6 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
             Win o0, o1, o2;   // o2: a sibling left behind by chaining
             int no = 0;
             bool h2 = false;
-            FanPend pend{};
-            pend.enabled = true;
             if (wi < nwS) {
                 const unsigned int i = (wi << 5) + lane;
                 if (i < nS) {
@@ -1467,7 +1445,7 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
                     // (key <= t_{i+1}) is propagated right away by the same
                     // thread, up to p.chain propagations
                     for (int step = 1;; ++step) {
-                        no = propagate(p, sg, it, fsink, pend, win, o0, o1, ls);
+                        no = propagate(p, sg, it, fsink, win, o0, o1, ls);
                         if (no > maxchild) maxchild = no;
                         if (step >= p.chain || no == 0) break;
                         const bool c0ok = o0.key <= tn, c1ok = no > 1 && o1.key <= tn;
@@ -1516,7 +1494,18 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
                     // fans out on its own)
                     FanSpan f;
                     const bool span = fan_span(p, e.v, e.anchor, rel, false, f);
-                    if (dv == hi && pk.x == hi && pk.y == lo && span) {
+                    // still the vertex's distance and either the pick, or
+                    // better than a stale pick (our claim lost a race to a
+                    // worse candidate): the group's first lane claims it
+                    // now; a tie racing the same repair may fan out twice
+                    // (duplicate windows, never a missing fan)
+                    const bool stale = dv == hi && (pk.x > hi || (pk.x == hi && pk.y > lo));
+                    bool won = false;
+                    if (stale && sl == 0) won = cas_min_u128(T.pick + e.v, hi, lo, pk);
+                    const unsigned int gmask = FAN_LANES == 32 ? 0xffffffffu
+                                                                : ((1u << FAN_LANES) - 1u) << (lane & ~(FAN_LANES - 1));
+                    won = __shfl_sync(gmask, won, lane & ~(FAN_LANES - 1));
+                    if (dv == hi && ((pk.x == hi && pk.y == lo) || won) && span) {
                         if (sl == 0) ls.add(ST_FANS);
                         const int items = f.m * f.reps;
                         if (sl < items)
@@ -1565,7 +1554,6 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
             if (h2) put_at(s2, s2 ? sa : pa, o2);
             ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
             if (p.trace && wi < nwS) trace_max_warp(p, it, TR_ROUTED);
-            pend.complete();
             if (p.trace && wi < nwS) trace_max_warp(p, it, TR_SCAN_END);
             if (++iters_since_fold == FOLD_TRIPS) {
                 ls.fold();

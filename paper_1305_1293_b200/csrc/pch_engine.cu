@@ -157,9 +157,9 @@ __device__ __forceinline__ double unord64(unsigned long long b) {
 // spin and the closing __syncthreads (used to read the iteration's
 // counters once per CTA).  A waiter that sees no progress within 20 s
 // flags ERR_TIMEOUT instead of hanging.
-template <typename After>
+template <bool LeadingSync = true, typename After>
 __device__ __forceinline__ void grid_barrier(Ctrl *c, unsigned int &gen, After &&after) {
-    __syncthreads();
+    if (LeadingSync) __syncthreads();
     if (threadIdx.x == 0) {
         gen += 1;
         const unsigned int target = gen * gridDim.x;
@@ -1579,7 +1579,9 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
                 if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
             }
         }
-        grid_barrier(ctrl, gen);
+        // the __syncthreads before the publish already ordered every
+        // thread's outputs before thread 0's release
+        grid_barrier<false>(ctrl, gen, [] {});
         // the next iteration's inputs: S_{i+1}, P_{i+1} (parity par^1) and
         // the fan candidates of iteration i (parity par); the counts and
         // the controller's inputs are read in one round trip

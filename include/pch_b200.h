@@ -61,7 +61,8 @@ typedef struct pch_config {
     int32_t chain;           /* propagations one thread may chain per
                                 iteration: a child the next batch would
                                 select is propagated at once by the same
-                                thread (0 = library default 2, 1 = off;
+                                thread (0 = library default: 3 on meshes
+                                of >= 2^18 faces, else 2; 1 = off;
                                 one-barrier solver only) */
 } pch_config;
 

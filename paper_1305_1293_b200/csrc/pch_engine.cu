@@ -1857,8 +1857,12 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         // fields and batched rows alike; a third crossing pays on large
         // meshes (deep wavefronts), not on small ones where it only
         // lengthens the iteration (profiles/r01_controller.md)
+        // a fourth on anisotropic meshes (mean smallest face altitude below
+        // half a mean edge: a crossing advances less distance there)
         p.chain = cfg->chain > 0 ? cfg->chain
-                                 : (m->nhe / 3 >= LONG_CHAIN_FACES ? DEFAULT_CHAIN + 1 : DEFAULT_CHAIN);
+                                 : (m->nhe / 3 >= LONG_CHAIN_FACES
+                                        ? DEFAULT_CHAIN + 1 + (m->mean_alt < 0.5 * m->mean_edge ? 1 : 0)
+                                        : DEFAULT_CHAIN);
         if (const char *ch = getenv("PCH_CHAIN")) p.chain = std::max(1, atoi(ch));  // development
         p.delta0 = m->mean_edge;
         // skinny faces (torus-knot tubes): a step of several face

@@ -53,7 +53,8 @@ class EngineConfig:
     ``chain`` bounds how many propagations one thread performs per
     iteration when a child falls inside the next batch's threshold (it is
     then propagated at once instead of waiting for the next iteration);
-    0 = library default (3 on meshes of >= 2^18 faces, else 2), 1 = off.
+    0 = library default (3 on meshes of >= 2^18 faces, 4 if their faces
+    are anisotropic, else 2), 1 = off.
     """
 
     k: int = 16384

@@ -1727,6 +1727,8 @@ struct pch_mesh {
     Params prm{};
     int64_t *d_src = nullptr;
     size_t src_cap = 0;
+    char *fps_buf = nullptr;  // farthest-point sampling scratch (grows)
+    size_t fps_cap = 0;
     double *d_out = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
@@ -2220,6 +2222,7 @@ int pch_mesh_destroy(pch_mesh *m) {
     cudaFree(m->fanhdr);
     cudaFree(m->anchor_wlo);
     cudaFree(m->d_src);
+    cudaFree(m->fps_buf);
     cudaFree(m->d_out);
     cudaFree(m->trace);
     if (m->ev0) cudaEventDestroy(m->ev0);
@@ -2308,9 +2311,16 @@ int pch_fps(pch_mesh *m, int64_t first, int64_t n_samples, const pch_config *cfg
     constexpr int NB = 4 * 148;  // argmax stage-1 blocks
     const size_t need = sizeof(int64_t) * n_samples + sizeof(double) * m->nv +
                         NB * (sizeof(double) + sizeof(long long));
-    // samples, the running min-field and the argmax scratch in one buffer
-    char *buf = nullptr;
-    CK(cudaMalloc(&buf, need));
+    // samples, the running min-field and the argmax scratch in one buffer,
+    // kept with the mesh (no allocation / implicit sync per call)
+    if (need > m->fps_cap) {
+        cudaFree(m->fps_buf);
+        m->fps_buf = nullptr;
+        m->fps_cap = 0;
+        CK(cudaMalloc(&m->fps_buf, need));
+        m->fps_cap = need;
+    }
+    char *buf = m->fps_buf;
     int64_t *d_samples = reinterpret_cast<int64_t *>(buf);
     double *d_min = reinterpret_cast<double *>(buf + sizeof(int64_t) * n_samples);
     double *d_bd = d_min + m->nv;
@@ -2318,7 +2328,6 @@ int pch_fps(pch_mesh *m, int64_t first, int64_t n_samples, const pch_config *cfg
     cudaStream_t st = m->stream;
     auto done = [&](int code) {
         cudaStreamSynchronize(st);
-        cudaFree(buf);
         return code;
     };
     if (cudaMemcpyAsync(d_samples, &first, sizeof(int64_t), cudaMemcpyHostToDevice, st) != cudaSuccess)

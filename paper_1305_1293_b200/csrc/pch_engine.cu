@@ -359,6 +359,7 @@ constexpr int TPB = PCH_TPB;      // threads per CTA of every solver kernel
 constexpr int NWARP = TPB / 32;
 constexpr double DELTA_FLOOR = 0.45;  // controller step floor, mean edge lengths
 constexpr double DELTA_CAP = 0.75;    // controller step cap, mean edge lengths
+constexpr double DELTA_CAP_LONG = 0.6;  // ... with chains longer than DEFAULT_CHAIN
 constexpr double ALT_FLOOR = 1.0;     // ... and floor <= this many mean face altitudes
 constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more crossing
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
@@ -1872,7 +1873,9 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         // The bounds are per two crossings and scale with the chain length.
         const double per_cross = 0.5 * p.chain;
         p.delta_min = per_cross * std::min(DELTA_FLOOR * m->mean_edge, ALT_FLOOR * m->mean_alt);
-        p.delta_max = per_cross * DELTA_CAP * m->mean_edge;
+        // long chains select deeper per iteration: a tighter cap keeps the
+        // out-of-order share down (profiles/r01_controller.md)
+        p.delta_max = per_cross * (p.chain > DEFAULT_CHAIN ? DELTA_CAP_LONG : DELTA_CAP) * m->mean_edge;
         if (const char *fd = getenv("PCH_DELTA")) {  // development: fixed step
             const double dlt = atof(fd) * m->mean_edge;
             if (dlt > 0.0) p.delta0 = p.delta_min = p.delta_max = dlt;

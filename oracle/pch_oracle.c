@@ -631,7 +631,6 @@ int pch_oracle_run_pch(const int64_t *origin, const int64_t *opposite,
                        int64_t k, int workers, int strided, double eps_win,
                        int fan_full, int64_t max_iterations, double *dist,
                        ostats *st) {
-    const double eps_num = 1e-12;
     omesh m = {origin, opposite, length, corner, vclass, nv, 3 * nf};
     memset(st, 0, sizeof(*st));
     for (int64_t v = 0; v < nv; ++v) dist[v] = INFINITY;

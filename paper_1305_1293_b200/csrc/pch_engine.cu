@@ -364,7 +364,7 @@ constexpr double ALT_FLOOR = 1.0;     // ... and floor <= this many mean face al
 constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more crossing
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
-constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together
+constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together (at most)
 constexpr int MAX_CTAS = 1024;        // chunk-count tables of the live solver
 constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
@@ -1729,6 +1729,7 @@ struct pch_mesh {
     int64_t *d_src = nullptr;
     size_t src_cap = 0;
     char *fps_buf = nullptr;  // farthest-point sampling scratch (grows)
+    size_t ws_bytes = 0;      // bytes held by the solve workspace
     size_t fps_cap = 0;
     double *d_out = nullptr;
     cudaStream_t stream = nullptr;
@@ -1749,6 +1750,7 @@ static void free_ws(pch_mesh *m) {
     for (void *q : m->ws) cudaFree(q);
     m->ws.clear();
     m->cap = 0;
+    m->ws_bytes = 0;
 }
 
 template <typename T>
@@ -1756,6 +1758,7 @@ static int ws_alloc(pch_mesh *m, T **out, size_t count) {
     void *q = nullptr;
     cudaError_t e = cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T));
     if (e != cudaSuccess) return fail(PCH_ERR_NOMEM, std::string("cudaMalloc workspace: ") + cudaGetErrorString(e));
+    m->ws_bytes += std::max<size_t>(count, 1) * sizeof(T);
     m->ws.push_back(q);
     *out = static_cast<T *>(q);
     return PCH_OK;
@@ -2293,6 +2296,19 @@ int pch_run_rows(pch_mesh *m, const int64_t *sources, int64_t n_sources, const p
     // batches of R fields solved together (one field per source); the
     // deterministic solver runs them one at a time
     int R = (cfg->flags & PCH_FLAG_DETERMINISTIC) ? 1 : DEFAULT_ROWS;
+    // and no more than half the device memory can hold: per row the
+    // distance / split / pick tables, per 4 rows one base window capacity
+    // (4 window SoA buffers, event lists, fan candidates; ensure_ws)
+    if (R > 1 && cfg->pool_capacity <= 0) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const double budget = 0.5 * (double)(free_b + m->ws_bytes);
+            const double per_row = 24.0 * m->nv + 16.0 * m->nhe;
+            const double base = (double)std::max<long long>(1 << 20, 2ll * m->nhe);
+            auto est = [&](int r) { return r * per_row + base * std::max(1, r / 4) * 472.0; };
+            while (R > 1 && est(R) > budget) R /= 2;
+        }
+    }
     if (const char *rr = getenv("PCH_ROWS")) R = std::max(1, atoi(rr));  // development
     for (int64_t r0 = 0; r0 < n_sources; r0 += R) {
         const int n = (int)std::min<int64_t>(R, n_sources - r0);

@@ -366,7 +366,7 @@ constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before 
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together (at most)
 constexpr int MAX_CTAS = 1024;        // chunk-count tables of the live solver
-constexpr int FAN_LANES = 16;     // lanes per saddle fan (wedges x repetitions)
+constexpr int FAN_LANES = 8;      // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
 constexpr int FE_CAP = 2 * TPB;

@@ -16,6 +16,7 @@
  *                     (engine.py:433)
  *   pch_run_device    the same with device-resident sources / output
  *   pch_run_rows      batched single-source fields, one row per source
+ *   pch_run_rows_device  the same with device-resident sources / rows
  *                     (the CLI's multi-source use, cli.py:382 context;
  *                      paper Table 3 "multiple-source-all-destination")
  *   pch_fps           farthest-point sampling on seeded single-source solves
@@ -36,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PCH_ABI_VERSION 2
+#define PCH_ABI_VERSION 3
 
 enum pch_status {
     PCH_OK = 0,
@@ -55,7 +56,9 @@ typedef struct pch_config {
                                 the device threshold selection) */
     int32_t fan_mode;        /* 0 clip, 1 full_edges */
     double epsilon_window;   /* tiny-window tolerance (default 1e-6) */
-    int64_t max_iterations;  /* <= 0: no cap */
+    int64_t max_iterations;  /* < 0: no cap (reference None); n >= 0: the
+                                solve fails with PCH_ERR_GUARD once it runs
+                                more than n iterations (engine.py:475) */
     int64_t pool_capacity;   /* initial window-pool capacity; 0 = auto */
     int32_t flags;           /* PCH_FLAG_* */
     int32_t chain;           /* propagations one thread may chain per
@@ -65,6 +68,8 @@ typedef struct pch_config {
                                 of >= 2^18 faces, 4 if they are
                                 anisotropic, else 2; 1 = off;
                                 one-barrier solver only) */
+    double time_limit_s;     /* device wall-time guard in seconds, 0 = none
+                                (no reference counterpart; PCH_ERR_GUARD) */
 } pch_config;
 
 #define PCH_FLAG_NO_RECHECK 1   /* disable the pop-time endpoint re-check */
@@ -96,6 +101,15 @@ typedef struct pch_stats {
     int64_t buffer_regrows;
     double time_total_ms;     /* device time of the solve (CUDA events) */
     double time_kernel_ms;    /* persistent-kernel time only */
+    /* RunStats.time_select / _propagate / _compact / _events
+     * (engine.py:470-473): the kernel time split by warp-cycle attribution
+     * (the phases are fused into one kernel; select = barrier, prefix
+     * rebuild and step controller; events = saddle fans and, in the
+     * deterministic solver, the table commit) */
+    double time_select_ms;
+    double time_propagate_ms;
+    double time_compact_ms;
+    double time_events_ms;
 } pch_stats;
 
 typedef struct pch_mesh pch_mesh;
@@ -136,6 +150,15 @@ int pch_run_device(pch_mesh *mesh, const int64_t *d_sources,
 int pch_run_rows(pch_mesh *mesh, const int64_t *sources, int64_t n_sources,
                  const pch_config *config, double *out_rows,
                  pch_stats *stats);
+
+/* pch_run_rows with device-resident sources (int64[n_sources]) and output
+ * (double[n_sources * n_vertices]) on the mesh's device; `stream` as in
+ * pch_run_device.  The rows never cross PCIe (multi-GPU gathers read them
+ * in place, paper_1305_1293_b200/shard.py).  An out-of-range device source
+ * returns PCH_ERR_SOURCE. */
+int pch_run_rows_device(pch_mesh *mesh, const int64_t *d_sources,
+                        int64_t n_sources, const pch_config *config,
+                        double *d_out_rows, void *stream, pch_stats *stats);
 
 /* Greedy farthest-point sampling (north star: batched multi-source
  * workloads): sample 0 is `first`, sample s+1 the vertex with the largest

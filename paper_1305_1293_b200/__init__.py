@@ -7,7 +7,7 @@ persistent sm_100a kernel behind the C ABI in ``include/pch_b200.h``.
 """
 from .engine import (DeviceMesh, EngineConfig, EngineGuard, RunStats,
                      device_mesh, farthest_point_sampling, run_pch,
-                     run_pch_device, run_pch_rows)
+                     run_pch_device, run_pch_rows, run_pch_rows_device)
 from .mesh import (BOUNDARY, MeshError, SurfaceMesh, VertexClass,
                    build_half_edge_mesh, classify_total_angle,
                    next_half_edge, prev_half_edge)
@@ -20,4 +20,5 @@ __all__ = [
     "classify_total_angle", "device_mesh", "farthest_point_sampling",
     "next_half_edge",
     "prev_half_edge", "run_pch", "run_pch_device", "run_pch_rows",
+    "run_pch_rows_device",
 ]

@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PCH_B200_LIB") or os.path.join(_HERE, "_lib", "libpch_b200.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 PCH_OK = 0
 PCH_ERR_CUDA = 1
@@ -35,7 +35,7 @@ class PchConfig(ctypes.Structure):
                 ("fan_mode", ctypes.c_int32), ("epsilon_window", ctypes.c_double),
                 ("max_iterations", ctypes.c_int64),
                 ("pool_capacity", ctypes.c_int64), ("flags", ctypes.c_int32),
-                ("chain", ctypes.c_int32)]
+                ("chain", ctypes.c_int32), ("time_limit_s", ctypes.c_double)]
 
 
 STAT_FIELDS = ("iterations", "windows_propagated", "total_windows_created",
@@ -46,16 +46,20 @@ STAT_FIELDS = ("iterations", "windows_propagated", "total_windows_created",
                "fans_emitted", "buffer_regrows")
 
 
+TIME_FIELDS = ("time_total_ms", "time_kernel_ms", "time_select_ms",
+               "time_propagate_ms", "time_compact_ms", "time_events_ms")
+
+
 class PchStats(ctypes.Structure):
     _fields_ = ([(f, ctypes.c_int64) for f in STAT_FIELDS]
-                + [("time_total_ms", ctypes.c_double),
-                   ("time_kernel_ms", ctypes.c_double)])
+                + [(f, ctypes.c_double) for f in TIME_FIELDS])
 
 
 # symbols declared in include/pch_b200.h
 EXPORTS = ("pch_abi_version", "pch_last_error", "pch_device_count",
            "pch_mesh_create", "pch_mesh_destroy", "pch_mesh_device_bytes",
-           "pch_run", "pch_run_device", "pch_run_rows", "pch_fps")
+           "pch_run", "pch_run_device", "pch_run_rows", "pch_run_rows_device",
+           "pch_fps")
 
 _lib = None
 
@@ -90,6 +94,9 @@ def load():
     lib.pch_run_rows.argtypes = [P, P, i64, ctypes.POINTER(PchConfig), P,
                                  ctypes.POINTER(PchStats)]
     lib.pch_run_rows.restype = ctypes.c_int
+    lib.pch_run_rows_device.argtypes = [P, P, i64, ctypes.POINTER(PchConfig), P, P,
+                                        ctypes.POINTER(PchStats)]
+    lib.pch_run_rows_device.restype = ctypes.c_int
     lib.pch_fps.argtypes = [P, i64, i64, ctypes.POINTER(PchConfig), P, P,
                             ctypes.POINTER(PchStats)]
     lib.pch_fps.restype = ctypes.c_int

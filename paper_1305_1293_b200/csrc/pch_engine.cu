@@ -52,9 +52,13 @@ enum { ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_PRUNE_TINY,
        ST_FANS, ST_MAXCHILD, ST_PEAK,
        // PCH_PROFILE section clocks (clock64 deltas summed over threads)
        ST_CYC_PROP, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
-       ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES, N_ST };
+       ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES,
+       // phase attribution of the one-barrier solver (warp cycles, lane 0):
+       // the reference's RunStats.time_select / _propagate / _compact /
+       // _events (engine.py:470-473) as shares of the kernel time
+       ST_PH_SELECT, ST_PH_PROP, ST_PH_COMPACT, ST_PH_EVENTS, N_ST };
 
-enum { ERR_NONE = 0, ERR_OVERFLOW = 1, ERR_GUARD = 2, ERR_TIMEOUT = 3 };
+enum { ERR_NONE = 0, ERR_OVERFLOW = 1, ERR_GUARD = 2, ERR_TIMEOUT = 3, ERR_SOURCE = 4 };
 
 struct Slot {                // per-iteration counters (ring of NSLOT)
     unsigned long long nS;   // size of the selected batch S
@@ -288,11 +292,15 @@ __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
 // shared counters every FOLD_TRIPS trips and at exit (one warp reduction
 // per field, one shared atomic per nonzero field from lane 0): a
 // shared-memory atomic per increment serialises the propagation path
-// (measured ~25% of the solve).  Per trip a thread adds at most 4 to any
-// field, so FOLD_TRIPS = 60 keeps every field below 256.  The others
-// (profiling clocks, maxima) and `direct` objects go straight to shared
-// memory.
-constexpr int FOLD_TRIPS = 60;
+// (measured ~25% of the solve).  A propagation adds at most 4 to any field
+// (3 distance + 1 angle event), a trip chains up to p.chain of them, so
+// folding every fold_trips(chain) = 255 / (4 chain) trips keeps every field
+// below 256.  The others (profiling clocks, maxima) and `direct` objects go
+// straight to shared memory.
+__host__ __device__ __forceinline__ int fold_trips(int chain) {
+    const int c = chain > 1 ? chain : 1;
+    return 255 / (4 * c) > 1 ? 255 / (4 * c) : 1;
+}
 struct LocalStats {
     unsigned long long *s;
     bool direct;
@@ -990,7 +998,11 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
     const int lane = threadIdx.x & 31;
     const unsigned long long t_start = globaltimer();
     int it = 0;
-    for (;;) {
+    // an initialisation failure (source-window overflow, invalid device
+    // source) leaves slot 0 unusable: every CTA reads the same flag before
+    // iteration 0 and skips the loop
+    const bool init_err = *(volatile int *)&ctrl->error != 0;
+    for (; !init_err;) {
         Slot &cur = ctrl->slot[it % 3];
         Slot &prev = ctrl->slot[(it + 2) % 3];
         Slot &nxt = ctrl->slot[(it + 1) % 3];
@@ -1004,6 +1016,14 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         }
 
         // ================= phase A: propagate =================
+        long long ph0 = clock64();
+        auto phase = [&](int which) {
+            if (threadIdx.x == 0) {
+                const long long now = clock64();
+                s_st[which] += (unsigned long long)(now - ph0);
+                ph0 = now;
+            }
+        };
         if (blockIdx.x == 0) {
             if (threadIdx.x < sizeof(Slot) / 8)
                 reinterpret_cast<unsigned long long *>(&nxt)[threadIdx.x] = 0ull;
@@ -1048,6 +1068,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 }
             }
         }
+        phase(ST_PH_PROP);
         // (A2) saddle fans of iteration it-1, one warp per fan event with the
         // lanes spread over the fan's wedges.  Only the event whose candidate
         // is the committed distance and wins the per-vertex pick (smallest
@@ -1097,12 +1118,14 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         }
         flush_hist(s_hist, hcur);
         if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_A_END);
+        phase(ST_PH_EVENTS);
         grid_barrier(ctrl, gen);
         if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0)
             p.trace[(size_t)it * TR_N + TR_B1] = globaltimer();
 
         // ================= phase B: organise =================
         Thresh th = pick_threshold(hcur, base, w, p.K);
+        phase(ST_PH_SELECT);
         {
             // commit the shadow tables for entries touched this iteration
             const unsigned long long nTV = *(volatile unsigned long long *)&cur.nTV;
@@ -1127,6 +1150,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                     p.fanpick[(it + 2) % 3][fe[i].v] = make_ulonglong2(~0ull, ~0ull);
             }
         }
+        phase(ST_PH_EVENTS);
         {
             // partition P_i + C_i -> S_{i+1} (key <= t) and P_{i+1}: stream
             // compaction with one reservation per CTA and trip per output
@@ -1165,11 +1189,12 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             flush_hist(s_hist, p.hist[(it + 1) & 1]);
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
-            if (p.max_iter > 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
+            if (p.max_iter >= 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
             if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
         }
         if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_B_END);
         grid_barrier(ctrl, gen);
+        phase(ST_PH_COMPACT);
 
         // ================= termination =================
         const int err = *(volatile int *)&ctrl->error;
@@ -1290,10 +1315,11 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
         s_nsp = 0ull;
         s_nf = 0u;
     }
-    LocalStats ls{s_st, false};   // packed per-thread counters, folded every FOLD_TRIPS
+    LocalStats ls{s_st, false};   // packed per-thread counters, folded every fold_every trips
     LocalStats lsd{s_st, true};   // rare paths: straight to shared memory
     int maxchild = 0;
     int iters_since_fold = 0;
+    const int fold_every = fold_trips(p.chain);
     const unsigned long long ch = (unsigned long long)p.cap / G;
     const unsigned long long chF = (unsigned long long)p.fancap / G;
     const unsigned long long gthreads = (unsigned long long)G * TPB;
@@ -1344,7 +1370,14 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
     };
     build_prefix(0, 1, &ctrl->slot[0]);  // S_0: the source windows (chunk-published by k_source_windows)
     int it = 0;
-    for (;;) {
+    // an initialisation failure (a source-window chunk overflowed, an
+    // invalid device source) makes the published counts meaningless: every
+    // CTA read the same flag with the prefix tables and skips the loop
+    const bool init_err = s_c[0] != 0ull;
+    // phase clocks (lane 0 of every warp): the iteration's barrier, prefix
+    // rebuild and controller count as selection of the next batch
+    long long ph_t = clock64();
+    for (; !init_err;) {
         const int par = it & 1;                     // parity of the iteration's inputs
         const unsigned int nS = s_pre[0][G], nP = s_pre[1][G], nF = it > 0 ? s_pre[2][G] : 0u;
         const unsigned long long pminb = s_c[1], smaxb = s_c[2];
@@ -1419,6 +1452,11 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
         const unsigned int nLw = (unsigned int)nwarps > nwS ? (unsigned int)nwarps - nwS : 0u;
         const bool split = nLw > 0u && nwF + nwP <= LIGHT_PER_WARP * nLw;
         const unsigned int wstep = !split ? (unsigned int)nwarps : ((unsigned int)gwid < nwS ? W : nLw);
+        if (lane == 0) {
+            const long long now = clock64();
+            atomicAdd(&s_st[ST_PH_SELECT], (unsigned long long)(now - ph_t));
+            ph_t = now;
+        }
         for (unsigned int wi = (unsigned int)gwid; wi < W; wi += wstep) {
             Win o0, o1, o2;   // o2: a sibling left behind by chaining
             int no = 0;
@@ -1525,6 +1563,12 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
             }
             // route: S_{i+1} if key <= t_{i+1}, else P_{i+1}
             __syncwarp();
+            if (lane == 0) {
+                const long long now = clock64();
+                atomicAdd(&s_st[wi < nwS ? ST_PH_PROP : wi < nwS + nwF ? ST_PH_EVENTS : ST_PH_COMPACT],
+                          (unsigned long long)(now - ph_t));
+                ph_t = now;
+            }
             const bool s0 = no > 0 && o0.key <= tn, s1 = no > 1 && o1.key <= tn;
             const bool k0 = no > 0 && !s0, k1 = no > 1 && !s1;
             const bool s2 = h2 && o2.key <= tn, k2 = h2 && !s2;
@@ -1556,7 +1600,12 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
             ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
             if (p.trace && wi < nwS) trace_max_warp(p, it, TR_ROUTED);
             if (p.trace && wi < nwS) trace_max_warp(p, it, TR_SCAN_END);
-            if (++iters_since_fold == FOLD_TRIPS) {
+            if (lane == 0) {
+                const long long now = clock64();
+                atomicAdd(&s_st[ST_PH_COMPACT], (unsigned long long)(now - ph_t));
+                ph_t = now;
+            }
+            if (++iters_since_fold >= fold_every) {
                 ls.fold();
                 iters_since_fold = 0;
             }
@@ -1576,7 +1625,7 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
             s_smax = 0ull;
             if (p.trace) trace_max(p, it, TR_A_END);
             if (blockIdx.x == 0) {
-                if (p.max_iter > 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
+                if (p.max_iter >= 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
                 if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
             }
         }
@@ -1643,6 +1692,12 @@ __global__ void k_set_sources(Params p, const int64_t *src, int nsrc) {
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < nsrc) {
         const int64_t s = src[i];
+        // device-resident source lists (pch_run_device) are validated
+        // here: an out-of-range index fails the solve with PCH_ERR_SOURCE
+        if (s < 0 || s >= p.nv) {
+            atomicExch(&p.ctrl->error, ERR_SOURCE);
+            return;
+        }
         const size_t r = p.rows > 1 ? (size_t)i : 0;
         if (!p.live) p.dist_cur[s] = 0.0;
         p.dist_new[r * p.nv + s] = 0ull;
@@ -1674,7 +1729,7 @@ __global__ void k_source_windows(Params p, const int64_t *src, int nsrc) {
         }
         ls.add(ST_STORED);
     };
-    if (i < nsrc) {
+    if (i < nsrc && src[i] >= 0 && src[i] < p.nv) {
         int32_t s = (int32_t)src[i];
         if ((__double_as_longlong(__ldg(&p.fanhdr[s].meta_bits)) >> 32) & 0x7fffffffll)
         {
@@ -1838,6 +1893,8 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
                         ? cfg->pool_capacity
                         : std::max<long long>(1 << 20, 2ll * m->nhe) * std::max(1, rows / 4);
     if (m->cap > cap) cap = m->cap;
+    // every per-CTA chunk of the live solver holds at least 8 windows
+    cap = std::max<long long>(cap, 8ll * m->grid_live);
     int regrows = 0;
     for (;;) {
         int rc = ensure_ws(m, cap, rows);
@@ -1847,8 +1904,8 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.K = cfg->k;
         p.eps_win = cfg->epsilon_window;
         p.w0 = m->mean_edge / 64.0;
-        p.max_iter = cfg->max_iterations;
-        p.time_limit_ns = 120ull * 1000000000ull;
+        p.max_iter = cfg->max_iterations;  // < 0: no cap (reference max_iterations=None)
+        p.time_limit_ns = cfg->time_limit_s > 0.0 ? (unsigned long long)(cfg->time_limit_s * 1e9) : ~0ull;
         p.fan_full = cfg->fan_mode == 1;
         p.recheck = (cfg->flags & PCH_FLAG_NO_RECHECK) ? 0 : 1;
         p.live = (cfg->flags & PCH_FLAG_DETERMINISTIC) ? 0 : 1;
@@ -1963,6 +2020,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         if (c.error == ERR_GUARD)
             return fail(PCH_ERR_GUARD, "iteration cap " + std::to_string(cfg->max_iterations) + " exceeded");
         if (c.error == ERR_TIMEOUT) return fail(PCH_ERR_GUARD, "device wall-time guard tripped");
+        if (c.error == ERR_SOURCE) return fail(PCH_ERR_SOURCE, "invalid source index in the device source list");
         if (stats) {
             float t_all = 0.f, t_k = 0.f;
             cudaEventElapsedTime(&t_all, m->ev0, m->ev2);
@@ -1986,6 +2044,16 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             stats->buffer_regrows += regrows;
             stats->time_total_ms += t_all;
             stats->time_kernel_ms += t_k;
+            // phase shares of the kernel time from the warp-cycle attribution
+            const double ph[4] = {(double)c.st[ST_PH_SELECT], (double)c.st[ST_PH_PROP],
+                                  (double)c.st[ST_PH_COMPACT], (double)c.st[ST_PH_EVENTS]};
+            const double phs = ph[0] + ph[1] + ph[2] + ph[3];
+            if (phs > 0.0) {
+                stats->time_select_ms += t_k * ph[0] / phs;
+                stats->time_propagate_ms += t_k * ph[1] / phs;
+                stats->time_compact_ms += t_k * ph[2] / phs;
+                stats->time_events_ms += t_k * ph[3] / phs;
+            }
         }
         return PCH_OK;
     }
@@ -2243,6 +2311,7 @@ int64_t pch_mesh_device_bytes(const pch_mesh *m) { return m ? (int64_t)m->mesh_b
 
 static int check_sources(const pch_mesh *m, const int64_t *sources, int64_t n) {
     if (n <= 0) return fail(PCH_ERR_SOURCE, "at least one source vertex is required");
+    if (n > INT_MAX) return fail(PCH_ERR_SOURCE, "too many sources");
     for (int64_t i = 0; i < n; ++i)
         if (sources[i] < 0 || sources[i] >= m->nv)
             return fail(PCH_ERR_SOURCE, "invalid source index " + std::to_string(sources[i]));
@@ -2277,6 +2346,7 @@ int pch_run_device(pch_mesh *m, const int64_t *d_sources, int64_t n_sources, con
                    double *d_out, void *stream, pch_stats *stats) {
     if (!m || !cfg || !d_out || !d_sources) return fail(PCH_ERR_CONFIG, "null argument");
     if (n_sources <= 0) return fail(PCH_ERR_SOURCE, "at least one source vertex is required");
+    if (n_sources > INT_MAX) return fail(PCH_ERR_SOURCE, "too many sources");
     CK(cudaSetDevice(m->device));
     cudaStream_t st = stream ? (cudaStream_t)stream : m->stream;
     int rc = solve(m, d_sources, (int)n_sources, cfg, st, stats);
@@ -2286,15 +2356,12 @@ int pch_run_device(pch_mesh *m, const int64_t *d_sources, int64_t n_sources, con
     return PCH_OK;
 }
 
-int pch_run_rows(pch_mesh *m, const int64_t *sources, int64_t n_sources, const pch_config *cfg,
-                 double *out_rows, pch_stats *stats) {
-    if (!m || !cfg || !out_rows) return fail(PCH_ERR_CONFIG, "null argument");
-    int rc = check_sources(m, sources, n_sources);
-    if (rc) return rc;
-    CK(cudaSetDevice(m->device));
-    if ((rc = stage_sources(m, sources, n_sources))) return rc;
-    // batches of R fields solved together (one field per source); the
-    // deterministic solver runs them one at a time
+// batches of R fields solved together (one field per source), each
+// batch's rows copied out (to the host or in place on the device) while
+// the next batch solves on the same stream
+static int run_rows(pch_mesh *m, const int64_t *d_sources, int64_t n_sources, const pch_config *cfg,
+                    double *out_rows, bool out_on_device, cudaStream_t st, pch_stats *stats) {
+    // the deterministic solver runs them one at a time
     int R = (cfg->flags & PCH_FLAG_DETERMINISTIC) ? 1 : DEFAULT_ROWS;
     // and no more than half the device memory can hold: per row the
     // distance / split / pick tables, per 4 rows one base window capacity
@@ -2310,14 +2377,35 @@ int pch_run_rows(pch_mesh *m, const int64_t *sources, int64_t n_sources, const p
         }
     }
     if (const char *rr = getenv("PCH_ROWS")) R = std::max(1, atoi(rr));  // development
+    const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
     for (int64_t r0 = 0; r0 < n_sources; r0 += R) {
         const int n = (int)std::min<int64_t>(R, n_sources - r0);
-        if ((rc = solve(m, m->d_src + r0, n, cfg, m->stream, stats, n))) return rc;
-        CK(cudaMemcpyAsync(out_rows + r0 * (int64_t)m->nv, field_ptr(m), sizeof(double) * m->nv * n,
-                           cudaMemcpyDeviceToHost, m->stream));
+        int rc = solve(m, d_sources + r0, n, cfg, st, stats, n);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(out_rows + r0 * (int64_t)m->nv, field_ptr(m), sizeof(double) * m->nv * n, kind, st));
     }
-    CK(cudaStreamSynchronize(m->stream));
+    CK(cudaStreamSynchronize(st));
     return PCH_OK;
+}
+
+int pch_run_rows(pch_mesh *m, const int64_t *sources, int64_t n_sources, const pch_config *cfg,
+                 double *out_rows, pch_stats *stats) {
+    if (!m || !cfg || !out_rows) return fail(PCH_ERR_CONFIG, "null argument");
+    int rc = check_sources(m, sources, n_sources);
+    if (rc) return rc;
+    CK(cudaSetDevice(m->device));
+    if ((rc = stage_sources(m, sources, n_sources))) return rc;
+    return run_rows(m, m->d_src, n_sources, cfg, out_rows, false, m->stream, stats);
+}
+
+int pch_run_rows_device(pch_mesh *m, const int64_t *d_sources, int64_t n_sources, const pch_config *cfg,
+                        double *d_out_rows, void *stream, pch_stats *stats) {
+    if (!m || !cfg || !d_out_rows || !d_sources) return fail(PCH_ERR_CONFIG, "null argument");
+    if (n_sources <= 0) return fail(PCH_ERR_SOURCE, "at least one source vertex is required");
+    if (n_sources > INT_MAX) return fail(PCH_ERR_SOURCE, "too many sources");
+    CK(cudaSetDevice(m->device));
+    cudaStream_t st = stream ? (cudaStream_t)stream : m->stream;
+    return run_rows(m, d_sources, n_sources, cfg, d_out_rows, true, st, stats);
 }
 
 int pch_fps(pch_mesh *m, int64_t first, int64_t n_samples, const pch_config *cfg, int64_t *out_samples,

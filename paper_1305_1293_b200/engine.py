@@ -15,6 +15,7 @@ device every call raises.
 from __future__ import annotations
 
 import ctypes
+import threading
 from dataclasses import dataclass, fields
 
 import numpy as np
@@ -55,6 +56,10 @@ class EngineConfig:
     then propagated at once instead of waiting for the next iteration);
     0 = library default (3 on meshes of >= 2^18 faces, 4 if their faces
     are anisotropic, else 2), 1 = off.
+    ``max_iterations`` has the reference's meaning (None: no cap; n: raise
+    ``EngineGuard`` once more than n iterations ran, engine.py:475);
+    ``time_limit_s`` is an optional device wall-time guard (0 = none; no
+    reference counterpart), also raising ``EngineGuard``.
     """
 
     k: int = 16384
@@ -69,6 +74,7 @@ class EngineConfig:
     pool_capacity: int = 0
     deterministic: bool = False
     chain: int = 0
+    time_limit_s: float = 0.0
 
     def __post_init__(self):
         if self.k < 1:
@@ -83,6 +89,8 @@ class EngineConfig:
             raise ValueError("epsilon_window must be > 0")
         if self.chain < 0:
             raise ValueError("chain must be >= 0")
+        if self.time_limit_s < 0:
+            raise ValueError("time_limit_s must be >= 0")
 
     def to_native(self) -> _native.PchConfig:
         c = _native.PchConfig()
@@ -90,11 +98,12 @@ class EngineConfig:
         c.selection_mode = SELECTION_MODES.index(self.selection_mode)
         c.fan_mode = FAN_MODES.index(self.fan_mode)
         c.epsilon_window = float(self.epsilon_window)
-        c.max_iterations = int(self.max_iterations or 0)
+        c.max_iterations = -1 if self.max_iterations is None else int(self.max_iterations)
         c.pool_capacity = int(self.pool_capacity)
         c.flags = ((0 if self.recheck else _native.FLAG_NO_RECHECK)
                    | (_native.FLAG_DETERMINISTIC if self.deterministic else 0))
         c.chain = int(self.chain)
+        c.time_limit_s = float(self.time_limit_s)
         return c
 
 
@@ -139,6 +148,12 @@ class RunStats:
         s.time_device_ms = float(st.time_total_ms)
         s.time_kernel_ms = float(st.time_kernel_ms)
         s.time_total = s.time_device_ms / 1e3
+        # the four phases are fused into one kernel: the device attributes
+        # its warp cycles to them (include/pch_b200.h pch_stats)
+        s.time_select = float(st.time_select_ms) / 1e3
+        s.time_propagate = float(st.time_propagate_ms) / 1e3
+        s.time_compact = float(st.time_compact_ms) / 1e3
+        s.time_events = float(st.time_events_ms) / 1e3
         return s
 
 
@@ -166,6 +181,10 @@ class DeviceMesh:
         self.device = device
         self.n_vertices = mesh.n_vertices
         self._lib = lib
+        # one solve at a time per device mesh: the native workspace (window
+        # pools, tables, stream) belongs to the mesh handle, and ctypes
+        # releases the GIL during the call
+        self.lock = threading.Lock()
 
     @property
     def device_bytes(self) -> int:
@@ -226,8 +245,9 @@ def run_pch(mesh: SurfaceMesh, sources, config: EngineConfig | None = None):
     out = np.empty(mesh.n_vertices, dtype=np.float64)
     st = _native.PchStats()
     cfg = config.to_native()
-    rc = dm._lib.pch_run(dm.handle, src.ctypes.data, len(src),
-                         ctypes.byref(cfg), out.ctypes.data, ctypes.byref(st))
+    with dm.lock:
+        rc = dm._lib.pch_run(dm.handle, src.ctypes.data, len(src),
+                             ctypes.byref(cfg), out.ctypes.data, ctypes.byref(st))
     _check(rc)
     return out, RunStats.from_native(st)
 
@@ -247,9 +267,10 @@ def run_pch_rows(mesh: SurfaceMesh, sources, config: EngineConfig | None = None)
     out = np.empty((len(src), mesh.n_vertices), dtype=np.float64)
     st = _native.PchStats()
     cfg = config.to_native()
-    rc = dm._lib.pch_run_rows(dm.handle, src.ctypes.data, len(src),
-                              ctypes.byref(cfg), out.ctypes.data,
-                              ctypes.byref(st))
+    with dm.lock:
+        rc = dm._lib.pch_run_rows(dm.handle, src.ctypes.data, len(src),
+                                  ctypes.byref(cfg), out.ctypes.data,
+                                  ctypes.byref(st))
     _check(rc)
     return out, RunStats.from_native(st)
 
@@ -274,8 +295,9 @@ def farthest_point_sampling(mesh: SurfaceMesh, n_samples: int, first: int = 0,
     out = np.empty(mesh.n_vertices, dtype=np.float64)
     st = _native.PchStats()
     cfg = config.to_native()
-    rc = dm._lib.pch_fps(dm.handle, first, n, ctypes.byref(cfg), samples.ctypes.data,
-                         out.ctypes.data, ctypes.byref(st))
+    with dm.lock:
+        rc = dm._lib.pch_fps(dm.handle, first, n, ctypes.byref(cfg), samples.ctypes.data,
+                             out.ctypes.data, ctypes.byref(st))
     _check(rc)
     return samples, out, RunStats.from_native(st)
 
@@ -289,10 +311,31 @@ def run_pch_device(mesh: SurfaceMesh, d_sources_ptr: int, n_sources: int,
     dm = device_mesh(mesh, config.device)
     st = _native.PchStats()
     cfg = config.to_native()
-    rc = dm._lib.pch_run_device(dm.handle, ctypes.c_void_p(d_sources_ptr),
-                                int(n_sources), ctypes.byref(cfg),
-                                ctypes.c_void_p(d_out_ptr),
-                                ctypes.c_void_p(stream or None),
-                                ctypes.byref(st))
+    with dm.lock:
+        rc = dm._lib.pch_run_device(dm.handle, ctypes.c_void_p(d_sources_ptr),
+                                    int(n_sources), ctypes.byref(cfg),
+                                    ctypes.c_void_p(d_out_ptr),
+                                    ctypes.c_void_p(stream or None),
+                                    ctypes.byref(st))
+    _check(rc)
+    return RunStats.from_native(st)
+
+
+def run_pch_rows_device(mesh: SurfaceMesh, d_sources_ptr: int, n_sources: int,
+                        d_out_ptr: int, config: EngineConfig | None = None,
+                        stream: int = 0):
+    """Device-pointer rows (include/pch_b200.h pch_run_rows_device): sources
+    int64[n] and output float64[n, n_vertices] resident on the mesh's
+    device; the rows never cross PCIe (shard.py gathers them over NCCL)."""
+    config = config or EngineConfig()
+    dm = device_mesh(mesh, config.device)
+    st = _native.PchStats()
+    cfg = config.to_native()
+    with dm.lock:
+        rc = dm._lib.pch_run_rows_device(dm.handle, ctypes.c_void_p(d_sources_ptr),
+                                         int(n_sources), ctypes.byref(cfg),
+                                         ctypes.c_void_p(d_out_ptr),
+                                         ctypes.c_void_p(stream or None),
+                                         ctypes.byref(st))
     _check(rc)
     return RunStats.from_native(st)

@@ -37,7 +37,10 @@ def rel_dev():
 
 
 def golden_cases():
-    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz")))
+    """Reference-generated fixtures (make_golden.py); the large_* oracle
+    fixtures of the configuration meshes (make_large.py) are separate."""
+    return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
+                  if not os.path.basename(p).startswith("large_"))
 
 
 def load_golden(name):

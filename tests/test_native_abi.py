@@ -40,9 +40,9 @@ def test_library_loads_and_reports_abi():
 
 
 def test_struct_layouts_match_header():
-    # pch_config: 8+4+4+8+8+8+4+4 ; pch_stats: 17 int64 + 2 doubles
-    assert ctypes.sizeof(_native.PchConfig) == 48
-    assert ctypes.sizeof(_native.PchStats) == 8 * 19
+    # pch_config: 8+4+4+8+8+8+4+4+8 ; pch_stats: 17 int64 + 6 doubles
+    assert ctypes.sizeof(_native.PchConfig) == 56
+    assert ctypes.sizeof(_native.PchStats) == 8 * 23
 
 
 def test_sass_is_sm100a():
@@ -67,6 +67,12 @@ def test_engine_config_validation():
     assert (c.k, c.fan_mode, c.flags, c.chain) == (123, 1, _native.FLAG_NO_RECHECK, 3)
     c = EngineConfig(deterministic=True).to_native()
     assert c.flags == _native.FLAG_DETERMINISTIC
+    with pytest.raises(ValueError):
+        EngineConfig(time_limit_s=-1.0)
+    # reference semantics (engine.py:475): None = no cap, 0 = a real cap
+    assert EngineConfig().to_native().max_iterations == -1
+    assert EngineConfig(max_iterations=0).to_native().max_iterations == 0
+    assert EngineConfig(time_limit_s=2.5).to_native().time_limit_s == 2.5
 
 
 def test_source_validation_matches_reference(cube):

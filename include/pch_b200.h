@@ -70,6 +70,12 @@ typedef struct pch_config {
                                 one-barrier solver only) */
     double time_limit_s;     /* device wall-time guard in seconds, 0 = none
                                 (no reference counterpart; PCH_ERR_GUARD) */
+    double fan_margin;       /* saddle-fan interval widened by this angle
+                                (radians, [0, 0.1)) on both sides; 0 = the
+                                reference's clip (geom.py:239-256).  A small
+                                margin (1e-5) closes the rounding slivers
+                                between a fan and the straight windows
+                                passing its saddle */
 } pch_config;
 
 #define PCH_FLAG_NO_RECHECK 1   /* disable the pop-time endpoint re-check */
@@ -79,6 +85,16 @@ typedef struct pch_config {
                                      Algorithm 1 with its delayed updates);
                                      default is the one-barrier solver with
                                      live tables, equal to rounding */
+#define PCH_FLAG_ABSOLUTE_TINY 4  /* the reference's absolute tiny-window
+                                     drop (width <= epsilon_window,
+                                     geom.py:133) everywhere; default: the
+                                     threshold scales with the distance to
+                                     the pseudo source within 40 mean edges
+                                     (an angular width of eps/40 edges), so
+                                     the thin fan of a nearly flat saddle is
+                                     not dropped -- the reference's holes
+                                     and detoured vertices behind such
+                                     saddles */
 
 /* RunStats (engine.py:76) plus device-side counters. */
 typedef struct pch_stats {

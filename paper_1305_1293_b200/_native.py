@@ -24,6 +24,7 @@ PCH_ERR_NOMEM = 6
 
 FLAG_NO_RECHECK = 1
 FLAG_DETERMINISTIC = 2
+FLAG_ABSOLUTE_TINY = 4
 
 
 class NativeUnavailable(RuntimeError):
@@ -35,7 +36,8 @@ class PchConfig(ctypes.Structure):
                 ("fan_mode", ctypes.c_int32), ("epsilon_window", ctypes.c_double),
                 ("max_iterations", ctypes.c_int64),
                 ("pool_capacity", ctypes.c_int64), ("flags", ctypes.c_int32),
-                ("chain", ctypes.c_int32), ("time_limit_s", ctypes.c_double)]
+                ("chain", ctypes.c_int32), ("time_limit_s", ctypes.c_double),
+                ("fan_margin", ctypes.c_double)]
 
 
 STAT_FIELDS = ("iterations", "windows_propagated", "total_windows_created",

@@ -112,6 +112,8 @@ struct Params {
     // config
     long long K;
     double eps_win;
+    double inv_r0;             // 1 / radius of the angular tiny-window rule (huge: absolute)
+    double fan_widen;          // saddle-fan interval widened by this angle on both sides
     double w0;
     double delta0, delta_min, delta_max;  // one-barrier step controller
     long long max_iter;
@@ -372,7 +374,8 @@ constexpr double ALT_FLOOR = 1.0;     // ... and floor <= this many mean face al
 constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more crossing
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
-constexpr int DEFAULT_ROWS = 32;      // fields pch_run_rows solves together (at most)
+constexpr int DEFAULT_ROWS = 32;
+constexpr double TINY_R0_EDGES = 40.0;  // angular tiny-window radius, mean edge lengths      // fields pch_run_rows solves together (at most)
 constexpr int MAX_CTAS = 1024;        // chunk-count tables of the live solver
 constexpr int FAN_LANES = 8;      // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
@@ -591,8 +594,8 @@ __device__ __forceinline__ bool fan_span(const Params &p, int32_t v, int32_t anc
     }
     double width = f.theta - TWO_PI_D;
     if (width <= EPS_NUM) return false;
-    f.flo = aphi + rel + PI_D;
-    f.fhi = f.flo + width;
+    f.flo = aphi + rel + PI_D - p.fan_widen;
+    f.fhi = f.flo + width + 2.0 * p.fan_widen;
     if (interior) {
         double k = floor(f.flo / f.theta);
         f.flo -= k * f.theta;
@@ -655,7 +658,7 @@ __device__ __forceinline__ void fan_item(const Params &p, const RowTabs &t, uint
     Win c;
     int fate = make_child(__ldg(&fr.che), __ldg(&fr.cho), cv0, cv1, __ldg(&fr.capx), __ldg(&fr.lc), px, py,
                           qx, qy, s0, s1, 0.0, 0.0, cand,
-                          gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, c);
+                          gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, p.inv_r0, c);
     c.row = row;
     if (fate == CH_STORED) {
         emit(c);
@@ -783,10 +786,10 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     Win cl, cr;
     const int fl = make_child(3 * (fr / 3) + a1, cho_l, v0f, vdf, apx_l, lan, 0.0, 0.0, dx, dy, rA,
                               occ ? 1.0 : rB,
-                              ix, iy, dps, g0, gdd, g1, ell, 0.0, true, p.eps_win, cl);
+                              ix, iy, dps, g0, gdd, g1, ell, 0.0, true, p.eps_win, p.inv_r0, cl);
     const int frr = make_child(3 * (fr / 3) + a2, cho_r, vdf, v1f, apx_r, lpv, dx, dy, ell, 0.0,
                                occ ? 0.0 : rA, rB,
-                               ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, cr);
+                               ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, p.inv_r0, cr);
     cl.row = cr.row = w.row;
     // one-angle-one-split (Fig. 4a): a stored window that already gives
     // the apex a shorter distance leaves only the child on our side
@@ -1884,6 +1887,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
                  cudaStream_t st, pch_stats *stats, int rows = 1, const double *d_seed = nullptr) {
     if (cfg->k < 1) return fail(PCH_ERR_CONFIG, "k must be >= 1");
     if (!(cfg->epsilon_window > 0.0)) return fail(PCH_ERR_CONFIG, "epsilon_window must be > 0");
+    if (!(cfg->fan_margin >= 0.0 && cfg->fan_margin < 0.1)) return fail(PCH_ERR_CONFIG, "fan_margin must be in [0, 0.1)");
     if (cfg->fan_mode != 0 && cfg->fan_mode != 1) return fail(PCH_ERR_CONFIG, "fan_mode must be clip or full_edges");
     if (cfg->chain < 0) return fail(PCH_ERR_CONFIG, "chain must be >= 0");
     if (rows > 1 && (cfg->flags & PCH_FLAG_DETERMINISTIC))
@@ -1903,6 +1907,12 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.seed = d_seed;
         p.K = cfg->k;
         p.eps_win = cfg->epsilon_window;
+        // angular tiny-window rule within 40 mean edges of the pseudo
+        // source (pch_device.cuh make_child); the flag restores geom.py:133
+        p.inv_r0 = (cfg->flags & PCH_FLAG_ABSOLUTE_TINY) ? 1e300 : 1.0 / (TINY_R0_EDGES * m->mean_edge);
+        if (const char *r0 = getenv("PCH_TINY_R0"))  // development: radius in mean edges
+            if (!(cfg->flags & PCH_FLAG_ABSOLUTE_TINY)) p.inv_r0 = 1.0 / (atof(r0) * m->mean_edge);
+        p.fan_widen = cfg->fan_margin;
         p.w0 = m->mean_edge / 64.0;
         p.max_iter = cfg->max_iterations;  // < 0: no cap (reference max_iterations=None)
         p.time_limit_ns = cfg->time_limit_s > 0.0 ? (unsigned long long)(cfg->time_limit_s * 1e9) : ~0ull;

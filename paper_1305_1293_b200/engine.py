@@ -25,6 +25,7 @@ from .mesh import SurfaceMesh
 
 SELECTION_MODES = ("exact", "approximate_strided")
 FAN_MODES = ("clip", "full_edges")
+TINY_RULES = ("angular", "absolute")
 
 
 class EngineGuard(RuntimeError):
@@ -60,6 +61,15 @@ class EngineConfig:
     ``EngineGuard`` once more than n iterations ran, engine.py:475);
     ``time_limit_s`` is an optional device wall-time guard (0 = none; no
     reference counterpart), also raising ``EngineGuard``.
+    ``tiny_rule`` selects the tiny-window drop: "absolute" is the
+    reference's (width <= epsilon_window, geom.py:133); the default
+    "angular" scales the threshold with the distance to the pseudo source
+    within 40 mean edges, so the thin fans of nearly flat saddles survive
+    (the reference's rounding holes behind such saddles).
+    ``fan_margin`` widens every saddle fan by that angle (radians) on both
+    sides; 0 is the reference's clip.  With ``deterministic=True`` a margin
+    of 1e-5 removes the remaining rounding slivers on the 4M-face torus
+    knot.
     """
 
     k: int = 16384
@@ -75,6 +85,8 @@ class EngineConfig:
     deterministic: bool = False
     chain: int = 0
     time_limit_s: float = 0.0
+    tiny_rule: str = "angular"
+    fan_margin: float = 0.0
 
     def __post_init__(self):
         if self.k < 1:
@@ -91,6 +103,10 @@ class EngineConfig:
             raise ValueError("chain must be >= 0")
         if self.time_limit_s < 0:
             raise ValueError("time_limit_s must be >= 0")
+        if not 0.0 <= self.fan_margin < 0.1:
+            raise ValueError("fan_margin must be in [0, 0.1)")
+        if self.tiny_rule not in TINY_RULES:
+            raise ValueError(f"tiny_rule must be one of {TINY_RULES}")
 
     def to_native(self) -> _native.PchConfig:
         c = _native.PchConfig()
@@ -101,9 +117,11 @@ class EngineConfig:
         c.max_iterations = -1 if self.max_iterations is None else int(self.max_iterations)
         c.pool_capacity = int(self.pool_capacity)
         c.flags = ((0 if self.recheck else _native.FLAG_NO_RECHECK)
-                   | (_native.FLAG_DETERMINISTIC if self.deterministic else 0))
+                   | (_native.FLAG_DETERMINISTIC if self.deterministic else 0)
+                   | (_native.FLAG_ABSOLUTE_TINY if self.tiny_rule == "absolute" else 0))
         c.chain = int(self.chain)
         c.time_limit_s = float(self.time_limit_s)
+        c.fan_margin = float(self.fan_margin)
         return c
 
 

@@ -18,6 +18,11 @@ here and the fixtures are committed:
                oracle distances
     n_finite, finite_sum   count and sum of the finite distances
     windows    oracle windows created (ICH)
+    holes_full, val_full, windows_full
+               the same with the reference's fan_mode="full_edges" (every
+               saddle wedge emitted un-clipped, EngineConfig.fan_mode,
+               reference engine.py:57): no thin-fan rounding holes, the
+               field the default mode approximates where it has holes
 
 The full fields go to scratch/ (git-ignored) for development diagnostics.
 """
@@ -67,20 +72,32 @@ def make(case):
     elif src == "centre":
         src = centre_source(m)
     t = time.time()
-    d, st = O.run_ich(m, [src])
+    cached = os.path.join(ROOT, "scratch", f"ich_{name}.npy")
+    if os.path.exists(cached) and os.environ.get("REUSE_CLIP"):
+        d, st = np.load(cached), None
+    else:
+        d, st = O.run_ich(m, [src])
+    dfull, stf = O.run_ich(m, [src], fan_mode="full_edges")
     dt = time.time() - t
     nsamp = 16384 if "_row" in name else 32768
     rng = np.random.default_rng(20260)
     idx = np.sort(rng.choice(m.n_vertices, min(nsamp, m.n_vertices), replace=False)).astype(np.int32)
     fin = np.isfinite(d)
+    old = os.path.join(HERE, f"large_{name}.npz")
+    windows = (st["total_windows_created"] if st else int(np.load(old)["windows"]))
     rec = dict(mesh=np.array(mesh), mesh_sig=mesh_sig(m), source=np.int64(src),
                holes=np.flatnonzero(~fin).astype(np.int32), idx=idx, val=d[idx],
                n_finite=np.int64(fin.sum()), finite_sum=np.float64(np.sum(d[fin])),
-               windows=np.int64(st["total_windows_created"]))
+               windows=np.int64(windows),
+               holes_full=np.flatnonzero(~np.isfinite(dfull)).astype(np.int32),
+               val_full=dfull[idx], windows_full=np.int64(stf["total_windows_created"]))
     np.savez_compressed(os.path.join(HERE, f"large_{name}.npz"), **rec)
     os.makedirs(os.path.join(ROOT, "scratch"), exist_ok=True)
     np.save(os.path.join(ROOT, "scratch", f"ich_{name}.npy"), d)
-    return f"{name}: src={src} V={m.n_vertices} holes={int((~fin).sum())} windows={st['total_windows_created']} ich {dt:.1f}s"
+    np.save(os.path.join(ROOT, "scratch", f"ichfull_{name}.npy"), dfull)
+    return (f"{name}: src={src} V={m.n_vertices} holes={int((~fin).sum())} "
+            f"holes_full={int((~np.isfinite(dfull)).sum())} windows={windows} "
+            f"full={stf['total_windows_created']} ich {dt:.1f}s")
 
 
 def main():

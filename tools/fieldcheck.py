@@ -32,7 +32,7 @@ def parse(v):
             kw[k] = bool(int(x))
         elif k in ("chain", "k", "pool_capacity"):
             kw[k] = int(x)
-        elif k == "fan_mode":
+        elif k in ("fan_mode", "tiny_rule"):
             kw[k] = x
         else:
             kw[k] = float(x)
@@ -54,8 +54,28 @@ def compare(d, ref):
             "gpu_only_ids": np.flatnonzero(~fd & fr)[:20].tolist()}
 
 
+def rows_main(cases, variants):
+    """--rows CASE... : one run_pch_rows over the cases' sources (same mesh)."""
+    from paper_1305_1293_b200 import EngineConfig, meshes, run_pch_rows
+    gs = [dict(np.load(os.path.join(ROOT, "tests", "golden", f"large_{c}.npz"))) for c in cases]
+    m = meshes.bench_mesh(str(gs[0]["mesh"]))
+    src = [int(g["source"]) for g in gs]
+    for v in variants:
+        rows, st = run_pch_rows(m, src, EngineConfig(**parse(v)))
+        for c, r in zip(cases, rows):
+            ref = np.load(os.path.join(ROOT, "scratch_gpu", f"ich_{c}.npy"))
+            rep = compare(r, ref)
+            print("rows", c, v, json.dumps(rep), flush=True)
+        if os.environ.get("FIELDCHECK_SAVE"):
+            np.save(os.path.join(ROOT, "gpurun_out", f"rows_{v.replace(',', '_').replace('=', '')}.npy"), rows)
+
+
 def main():
     from paper_1305_1293_b200 import EngineConfig, meshes, run_pch
+    if sys.argv[1] == "--rows":
+        cases = [a for a in sys.argv[2:] if "=" not in a and a != "base"]
+        variants = [a for a in sys.argv[2:] if "=" in a or a == "base"] or ["base"]
+        return rows_main(cases, variants)
     case = sys.argv[1]
     variants = sys.argv[2:] or ["base"]
     g = dict(np.load(os.path.join(ROOT, "tests", "golden", f"large_{case}.npz")))
@@ -70,7 +90,8 @@ def main():
         rep["windows"] = st.total_windows_created
         out[v] = rep
         print(case, v, json.dumps(rep), flush=True)
-        np.save(os.path.join(ROOT, "gpurun_out", f"field_{case}_{v.replace(',', '_').replace('=', '')}.npy"), d)
+        if os.environ.get("FIELDCHECK_SAVE"):
+            np.save(os.path.join(ROOT, "gpurun_out", f"field_{case}_{v.replace(',', '_').replace('=', '')}.npy"), d)
     with open(os.path.join(ROOT, "gpurun_out", f"fieldcheck_{case}.json"), "w") as f:
         json.dump(out, f, indent=1)
 

@@ -85,6 +85,9 @@ typedef struct pch_config {
                                      Algorithm 1 with its delayed updates);
                                      default is the one-barrier solver with
                                      live tables, equal to rounding */
+#define PCH_FLAG_PHASE_TIMES 8  /* fill pch_stats.time_select/_propagate/
+                                     _compact/_events_ms and prop_item_us
+                                     (warp-cycle attribution, ~3 % slower) */
 #define PCH_FLAG_ABSOLUTE_TINY 4  /* the reference's absolute tiny-window
                                      drop (width <= epsilon_window,
                                      geom.py:133) everywhere; default: the
@@ -118,7 +121,8 @@ typedef struct pch_stats {
     double time_total_ms;     /* device time of the solve (CUDA events) */
     double time_kernel_ms;    /* persistent-kernel time only */
     /* RunStats.time_select / _propagate / _compact / _events
-     * (engine.py:470-473): the kernel time split by warp-cycle attribution
+     * (engine.py:470-473), with PCH_FLAG_PHASE_TIMES (else 0): the kernel
+     * time split by warp-cycle attribution
      * (the phases are fused into one kernel; select = barrier, prefix
      * rebuild and step controller; events = saddle fans and, in the
      * deterministic solver, the table commit) */
@@ -126,6 +130,10 @@ typedef struct pch_stats {
     double time_propagate_ms;
     double time_compact_ms;
     double time_events_ms;
+    /* (PCH_FLAG_PHASE_TIMES) mean duration of one batch work item of the one-barrier solver (a
+     * warp's chain of up to `chain` propagations), microseconds: the
+     * latency term of the solver's roofline */
+    double prop_item_us;
 } pch_stats;
 
 typedef struct pch_mesh pch_mesh;
@@ -175,6 +183,12 @@ int pch_run_rows(pch_mesh *mesh, const int64_t *sources, int64_t n_sources,
 int pch_run_rows_device(pch_mesh *mesh, const int64_t *d_sources,
                         int64_t n_sources, const pch_config *config,
                         double *d_out_rows, void *stream, pch_stats *stats);
+
+/* Roofline denominators measured on `device` (bench.py): out[0] = FP64
+ * FMA throughput in TFLOP/s (all SMs, independent chains), out[1] = one
+ * grid barrier of the live solver's cooperative grid in microseconds.
+ * n_out >= 2. */
+int pch_probe(int32_t device, double *out, int32_t n_out);
 
 /* Greedy farthest-point sampling (north star: batched multi-source
  * workloads): sample 0 is `first`, sample s+1 the vertex with the largest

@@ -25,6 +25,7 @@ PCH_ERR_NOMEM = 6
 FLAG_NO_RECHECK = 1
 FLAG_DETERMINISTIC = 2
 FLAG_ABSOLUTE_TINY = 4
+FLAG_PHASE_TIMES = 8
 
 
 class NativeUnavailable(RuntimeError):
@@ -49,7 +50,8 @@ STAT_FIELDS = ("iterations", "windows_propagated", "total_windows_created",
 
 
 TIME_FIELDS = ("time_total_ms", "time_kernel_ms", "time_select_ms",
-               "time_propagate_ms", "time_compact_ms", "time_events_ms")
+               "time_propagate_ms", "time_compact_ms", "time_events_ms",
+               "prop_item_us")
 
 
 class PchStats(ctypes.Structure):
@@ -61,7 +63,7 @@ class PchStats(ctypes.Structure):
 EXPORTS = ("pch_abi_version", "pch_last_error", "pch_device_count",
            "pch_mesh_create", "pch_mesh_destroy", "pch_mesh_device_bytes",
            "pch_run", "pch_run_device", "pch_run_rows", "pch_run_rows_device",
-           "pch_fps")
+           "pch_fps", "pch_probe")
 
 _lib = None
 
@@ -102,6 +104,8 @@ def load():
     lib.pch_fps.argtypes = [P, i64, i64, ctypes.POINTER(PchConfig), P, P,
                             ctypes.POINTER(PchStats)]
     lib.pch_fps.restype = ctypes.c_int
+    lib.pch_probe.argtypes = [ctypes.c_int32, P, ctypes.c_int32]
+    lib.pch_probe.restype = ctypes.c_int
     if lib.pch_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libpch_b200.so ABI version mismatch")
     _lib = lib

@@ -47,16 +47,17 @@ using namespace pch;
 // ---------------------------------------------------------------------------
 // device state
 
-enum { ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_PRUNE_TINY,
-       ST_PRUNE_DEGEN, ST_RECHECK, ST_STORED, ST_EV_CREATED, ST_EV_APPLIED,
-       ST_FANS, ST_MAXCHILD, ST_PEAK,
+enum { // the eight hot counters first: packed per thread (LocalStats)
+       ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_RECHECK, ST_STORED,
+       ST_EV_CREATED, ST_EV_APPLIED, ST_N_PACKED,
+       ST_PRUNE_TINY = ST_N_PACKED, ST_PRUNE_DEGEN, ST_FANS, ST_MAXCHILD, ST_PEAK,
        // PCH_PROFILE section clocks (clock64 deltas summed over threads)
        ST_CYC_PROP, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
        ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES,
        // phase attribution of the one-barrier solver (warp cycles, lane 0):
        // the reference's RunStats.time_select / _propagate / _compact /
        // _events (engine.py:470-473) as shares of the kernel time
-       ST_PH_SELECT, ST_PH_PROP, ST_PH_COMPACT, ST_PH_EVENTS, N_ST };
+       ST_PH_SELECT, ST_PH_PROP, ST_PH_COMPACT, ST_PH_EVENTS, ST_N_SITEM, N_ST };
 
 enum { ERR_NONE = 0, ERR_OVERFLOW = 1, ERR_GUARD = 2, ERR_TIMEOUT = 3, ERR_SOURCE = 4 };
 
@@ -114,6 +115,7 @@ struct Params {
     double eps_win;
     double inv_r0;             // 1 / radius of the angular tiny-window rule (huge: absolute)
     double fan_widen;          // saddle-fan interval widened by this angle on both sides
+    int phase;                 // attribute cycles to the four phases (PCH_FLAG_PHASE_TIMES)
     double w0;
     double delta0, delta_min, delta_max;  // one-barrier step controller
     long long max_iter;
@@ -289,47 +291,43 @@ __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
     return c;
 }
 
-// Run counters.  The hot ones (ST_PROPAGATED .. ST_FANS) are packed as
-// 8-bit fields into two per-thread registers and folded into the CTA's
-// shared counters every FOLD_TRIPS trips and at exit (one warp reduction
-// per field, one shared atomic per nonzero field from lane 0): a
-// shared-memory atomic per increment serialises the propagation path
-// (measured ~25% of the solve).  A propagation adds at most 4 to any field
-// (3 distance + 1 angle event), a trip chains up to p.chain of them, so
-// folding every fold_trips(chain) = 255 / (4 chain) trips keeps every field
-// below 256.  The others (profiling clocks, maxima) and `direct` objects go
-// straight to shared memory.
-__host__ __device__ __forceinline__ int fold_trips(int chain) {
-    const int c = chain > 1 ? chain : 1;
-    return 255 / (4 * c) > 1 ? 255 / (4 * c) : 1;
-}
+// Run counters.  The eight hot ones (ST_PROPAGATED .. ST_EV_APPLIED) are
+// packed as 16-bit fields into two per-thread registers and folded into
+// the CTA's shared counters when any field passes 2^15 and at exit (one
+// warp reduction per field, one shared atomic per nonzero field from lane
+// 0): a shared-memory atomic per increment serialises the propagation path
+// (measured ~25% of the solve).  A trip adds at most 4 per chained
+// propagation (3 distance + 1 angle event) to a field, far below the 2^15
+// headroom, so a fold is needed only every few thousand trips -- folding
+// on a fixed short period had cost 0.24 ms of the 1M-face field.  The rare
+// ones (tiny / degenerate prunes, fans), profiling clocks, maxima and
+// `direct` objects go straight to shared memory, only when nonzero.
 struct LocalStats {
     unsigned long long *s;
     bool direct;
     unsigned long long a = 0ull, b = 0ull;
     __device__ __forceinline__ void add(int i, unsigned long long x = 1ull) {
-        if (!direct && i <= ST_STORED) {
-            a += x << (8 * i);
-        } else if (!direct && i <= ST_FANS) {
-            b += x << (8 * (i - ST_EV_CREATED));
-        } else {
+        if (!direct && i <= 3) {
+            a += x << (16 * i);
+        } else if (!direct && i < ST_N_PACKED) {
+            b += x << (16 * (i - 4));
+        } else if (x) {
             atomicAdd(s + i, x);
         }
     }
     __device__ __forceinline__ void max(int i, unsigned long long x) { atomicMax(s + i, x); }
+    // some lane of the (converged) warp is past half of a field's range
+    __device__ __forceinline__ bool fold_due() const {
+        return __any_sync(0xffffffffu, ((a | b) & 0x8000800080008000ull) != 0ull);
+    }
     // fold the packed fields into shared memory (whole warp, converged):
     // one warp reduction per field, lane 0 adds the nonzero sums
     __device__ __forceinline__ void fold() {
         const int lane = threadIdx.x & 31;
 #pragma unroll
-        for (int k = 0; k <= ST_STORED; ++k) {
-            const unsigned int f = __reduce_add_sync(0xffffffffu, (unsigned int)((a >> (8 * k)) & 0xffull));
-            if (lane == 0 && f) atomicAdd(s + k, (unsigned long long)f);
-        }
-#pragma unroll
-        for (int k = ST_EV_CREATED; k <= ST_FANS; ++k) {
-            const unsigned int f =
-                __reduce_add_sync(0xffffffffu, (unsigned int)((b >> (8 * (k - ST_EV_CREATED))) & 0xffull));
+        for (int k = 0; k < ST_N_PACKED; ++k) {
+            const unsigned long long w = k <= 3 ? a : b;
+            const unsigned int f = __reduce_add_sync(0xffffffffu, (unsigned int)((w >> (16 * (k & 3))) & 0xffffull));
             if (lane == 0 && f) atomicAdd(s + k, (unsigned long long)f);
         }
         a = b = 0ull;
@@ -381,6 +379,7 @@ constexpr int FAN_LANES = 8;      // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
 constexpr int FE_CAP = 2 * TPB;
+
 
 struct Stage {
     unsigned int ntv, nte, nfe, pad;
@@ -1021,7 +1020,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         // ================= phase A: propagate =================
         long long ph0 = clock64();
         auto phase = [&](int which) {
-            if (threadIdx.x == 0) {
+            if (p.phase && threadIdx.x == 0) {
                 const long long now = clock64();
                 s_st[which] += (unsigned long long)(now - ph0);
                 ph0 = now;
@@ -1292,6 +1291,10 @@ __device__ __forceinline__ void warp_chunk_alloc2(unsigned long long *s_cnt, uns
 // fields and batched rows alike: a 2-CTA/SM build at 128 registers spilled
 // the propagation state to local memory and lost 9-16 % on batched rows
 // (profiles/r01_bigcheck.md)
+// PHASE: attribute warp cycles to the four phases (RunStats.time_*), on
+// request only (EngineConfig.phase_times): the clock reads and per-item
+// shared adds on the batch warps' critical path cost ~3 % of a field
+template <bool PHASE>
 __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
     // Outputs are chunked per CTA: CTA b writes the windows it routes to
     // slots [b*ch, (b+1)*ch) of the next batch / pool and its fan
@@ -1318,11 +1321,9 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
         s_nsp = 0ull;
         s_nf = 0u;
     }
-    LocalStats ls{s_st, false};   // packed per-thread counters, folded every fold_every trips
+    LocalStats ls{s_st, false};   // packed per-thread counters, folded when nearly full
     LocalStats lsd{s_st, true};   // rare paths: straight to shared memory
     int maxchild = 0;
-    int iters_since_fold = 0;
-    const int fold_every = fold_trips(p.chain);
     const unsigned long long ch = (unsigned long long)p.cap / G;
     const unsigned long long chF = (unsigned long long)p.fancap / G;
     const unsigned long long gthreads = (unsigned long long)G * TPB;
@@ -1455,7 +1456,7 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
         const unsigned int nLw = (unsigned int)nwarps > nwS ? (unsigned int)nwarps - nwS : 0u;
         const bool split = nLw > 0u && nwF + nwP <= LIGHT_PER_WARP * nLw;
         const unsigned int wstep = !split ? (unsigned int)nwarps : ((unsigned int)gwid < nwS ? W : nLw);
-        if (lane == 0) {
+        if (PHASE && lane == 0) {
             const long long now = clock64();
             atomicAdd(&s_st[ST_PH_SELECT], (unsigned long long)(now - ph_t));
             ph_t = now;
@@ -1566,10 +1567,11 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
             }
             // route: S_{i+1} if key <= t_{i+1}, else P_{i+1}
             __syncwarp();
-            if (lane == 0) {
+            if (PHASE && lane == 0) {
                 const long long now = clock64();
                 atomicAdd(&s_st[wi < nwS ? ST_PH_PROP : wi < nwS + nwF ? ST_PH_EVENTS : ST_PH_COMPACT],
                           (unsigned long long)(now - ph_t));
+                if (wi < nwS) atomicAdd(&s_st[ST_N_SITEM], 1ull);
                 ph_t = now;
             }
             const bool s0 = no > 0 && o0.key <= tn, s1 = no > 1 && o1.key <= tn;
@@ -1603,15 +1605,12 @@ __global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
             ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
             if (p.trace && wi < nwS) trace_max_warp(p, it, TR_ROUTED);
             if (p.trace && wi < nwS) trace_max_warp(p, it, TR_SCAN_END);
-            if (lane == 0) {
+            if (PHASE && lane == 0) {
                 const long long now = clock64();
                 atomicAdd(&s_st[ST_PH_COMPACT], (unsigned long long)(now - ph_t));
                 ph_t = now;
             }
-            if (++iters_since_fold >= fold_every) {
-                ls.fold();
-                iters_since_fold = 0;
-            }
+            if (ls.fold_due()) ls.fold();
         }
         // publish this CTA's outputs, then the grid barrier
         __syncthreads();
@@ -1793,6 +1792,7 @@ struct pch_mesh {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     int grid = 0, grid_live = 0;
+    double clock_mhz = 0.0;  // SM clock (cudaDevAttrClockRate) for cycle -> time
     unsigned long long *trace = nullptr;  // PCH_TRACE development timeline
     long long trace_cap = 0;
 };
@@ -1913,6 +1913,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         if (const char *r0 = getenv("PCH_TINY_R0"))  // development: radius in mean edges
             if (!(cfg->flags & PCH_FLAG_ABSOLUTE_TINY)) p.inv_r0 = 1.0 / (atof(r0) * m->mean_edge);
         p.fan_widen = cfg->fan_margin;
+        p.phase = (cfg->flags & PCH_FLAG_PHASE_TIMES) ? 1 : 0;
         p.w0 = m->mean_edge / 64.0;
         p.max_iter = cfg->max_iterations;  // < 0: no cap (reference max_iterations=None)
         p.time_limit_ns = cfg->time_limit_s > 0.0 ? (unsigned long long)(cfg->time_limit_s * 1e9) : ~0ull;
@@ -1982,7 +1983,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         void *args[] = {&p};
         if (p.live)
         {
-            const void *kern = (const void *)pch_live;
+            const void *kern = p.phase ? (const void *)pch_live<true> : (const void *)pch_live<false>;
             CK(cudaLaunchCooperativeKernel(kern, dim3(p.live_grid), dim3(TPB), args, 0, st));
         }
         else
@@ -2058,6 +2059,8 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             const double ph[4] = {(double)c.st[ST_PH_SELECT], (double)c.st[ST_PH_PROP],
                                   (double)c.st[ST_PH_COMPACT], (double)c.st[ST_PH_EVENTS]};
             const double phs = ph[0] + ph[1] + ph[2] + ph[3];
+            if (c.st[ST_N_SITEM] > 0 && m->clock_mhz > 0.0)
+                stats->prop_item_us = (double)c.st[ST_PH_PROP] / (double)c.st[ST_N_SITEM] / m->clock_mhz;
             if (phs > 0.0) {
                 stats->time_select_ms += t_k * ph[0] / phs;
                 stats->time_propagate_ms += t_k * ph[1] / phs;
@@ -2134,6 +2137,30 @@ __global__ void k_fps_argmax2(const double *bd_in, const long long *bv_in, int n
         }
     fps_warp_best(bd, bv);
     if (threadIdx.x == 0) *next = (int64_t)bv;
+}
+
+// ---------------------------------------------------------------------------
+// latency / peak probes (bench roofline denominators, pch_probe)
+
+// the solver's grid barrier alone, `n` times, on a cooperative grid shaped
+// like the live solver's
+__global__ void __launch_bounds__(TPB, 1) k_probe_barrier(Ctrl *c, int n) {
+    unsigned int gen = 0;
+    for (int i = 0; i < n; ++i) grid_barrier<true>(c, gen, [] {});
+}
+
+// FP64 FMA throughput: 8 independent dependent chains per thread
+__global__ void k_probe_fp64(double *out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 1234.5) out[0] = s;  // keeps the chains live
 }
 
 // ---------------------------------------------------------------------------
@@ -2285,10 +2312,12 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
         (e = cudaEventCreate(&m->ev0)) != cudaSuccess || (e = cudaEventCreate(&m->ev1)) != cudaSuccess ||
         (e = cudaEventCreate(&m->ev2)) != cudaSuccess)
         return cleanup(PCH_ERR_CUDA, std::string("stream/event: ") + cudaGetErrorString(e));
-    int nsm = 0, per_sm = 0, per_sm_live = 0;
+    int nsm = 0, per_sm = 0, per_sm_live = 0, khz = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device);
+    m->clock_mhz = khz / 1000.0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_persistent, TPB, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live, TPB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live<true>, TPB, 0);
     if (per_sm < 1 || per_sm_live < 1) return cleanup(PCH_ERR_CUDA, "persistent kernel cannot be resident");
     // persistent grids: every SM, as many co-resident CTAs as fit (<= 4)
     m->grid = nsm * std::min(per_sm, 4);
@@ -2318,6 +2347,49 @@ int pch_mesh_destroy(pch_mesh *m) {
 }
 
 int64_t pch_mesh_device_bytes(const pch_mesh *m) { return m ? (int64_t)m->mesh_bytes : 0; }
+
+int pch_probe(int32_t device, double *out, int32_t n_out) {
+    if (!out || n_out < 2) return fail(PCH_ERR_CONFIG, "pch_probe needs out[2]");
+    CK(cudaSetDevice(device));
+    int nsm = 0, per_sm = 0;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_live<true>, TPB, 0));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    double *buf = nullptr;
+    Ctrl *c = nullptr;
+    CK(cudaMalloc(&buf, 64));
+    CK(cudaMalloc(&c, sizeof(Ctrl)));
+    // FP64: 148 x 8 CTAs of 256 threads, 8 chains x iters FMAs each
+    const int iters = 1 << 14, blocks = nsm * 8;
+    k_probe_fp64<<<blocks, 256>>>(buf, 16, 1.0000001, 1e-9);  // warm-up
+    CK(cudaEventRecord(e0));
+    k_probe_fp64<<<blocks, 256>>>(buf, iters, 1.0000001, 1e-9);
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    out[0] = 2.0 * 8.0 * iters * blocks * 256.0 / (ms * 1e-3) / 1e12;  // TFLOP/s
+    // grid barrier at the live solver's grid
+    const int grid = nsm * std::min(std::max(per_sm, 1), 4), n = 2048;
+    int nn = n;
+    void *args[] = {&c, &nn};
+    CK(cudaMemset(c, 0, sizeof(Ctrl)));
+    CK(cudaLaunchCooperativeKernel((const void *)k_probe_barrier, dim3(grid), dim3(TPB), args, 0, 0));
+    CK(cudaMemset(c, 0, sizeof(Ctrl)));
+    CK(cudaEventRecord(e0));
+    CK(cudaLaunchCooperativeKernel((const void *)k_probe_barrier, dim3(grid), dim3(TPB), args, 0, 0));
+    CK(cudaEventRecord(e1));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    out[1] = ms * 1e3 / n;  // us per grid barrier
+    cudaFree(buf);
+    cudaFree(c);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return PCH_OK;
+}
 
 static int check_sources(const pch_mesh *m, const int64_t *sources, int64_t n) {
     if (n <= 0) return fail(PCH_ERR_SOURCE, "at least one source vertex is required");

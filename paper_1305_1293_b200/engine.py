@@ -69,7 +69,9 @@ class EngineConfig:
     ``fan_margin`` widens every saddle fan by that angle (radians) on both
     sides; 0 is the reference's clip.  With ``deterministic=True`` a margin
     of 1e-5 removes the remaining rounding slivers on the 4M-face torus
-    knot.
+    knot.  ``phase_times`` fills RunStats.time_select /
+    _propagate / _compact / _events (the four phases run fused in one
+    kernel; the device attributes its warp cycles to them, ~3 % slower).
     """
 
     k: int = 16384
@@ -87,6 +89,7 @@ class EngineConfig:
     time_limit_s: float = 0.0
     tiny_rule: str = "angular"
     fan_margin: float = 0.0
+    phase_times: bool = False
 
     def __post_init__(self):
         if self.k < 1:
@@ -118,7 +121,8 @@ class EngineConfig:
         c.pool_capacity = int(self.pool_capacity)
         c.flags = ((0 if self.recheck else _native.FLAG_NO_RECHECK)
                    | (_native.FLAG_DETERMINISTIC if self.deterministic else 0)
-                   | (_native.FLAG_ABSOLUTE_TINY if self.tiny_rule == "absolute" else 0))
+                   | (_native.FLAG_ABSOLUTE_TINY if self.tiny_rule == "absolute" else 0)
+                   | (_native.FLAG_PHASE_TIMES if self.phase_times else 0))
         c.chain = int(self.chain)
         c.time_limit_s = float(self.time_limit_s)
         c.fan_margin = float(self.fan_margin)
@@ -154,6 +158,7 @@ class RunStats:
     time_events: float = 0.0
     time_device_ms: float = 0.0
     time_kernel_ms: float = 0.0
+    prop_item_us: float = 0.0
 
     def to_dict(self) -> dict:
         return {f.name: getattr(self, f.name) for f in fields(self)}
@@ -172,6 +177,7 @@ class RunStats:
         s.time_propagate = float(st.time_propagate_ms) / 1e3
         s.time_compact = float(st.time_compact_ms) / 1e3
         s.time_events = float(st.time_events_ms) / 1e3
+        s.prop_item_us = float(st.prop_item_us)
         return s
 
 
@@ -357,3 +363,12 @@ def run_pch_rows_device(mesh: SurfaceMesh, d_sources_ptr: int, n_sources: int,
                                          ctypes.byref(st))
     _check(rc)
     return RunStats.from_native(st)
+
+
+def probe(device: int = 0) -> dict:
+    """Roofline denominators measured on the device (include/pch_b200.h
+    pch_probe): FP64 FMA TFLOP/s and the live solver's grid-barrier us."""
+    lib = _native.load()
+    out = (ctypes.c_double * 2)()
+    _check(lib.pch_probe(int(device), out, 2))
+    return {"fp64_tflops": float(out[0]), "grid_barrier_us": float(out[1])}

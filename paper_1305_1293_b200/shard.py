@@ -3,9 +3,10 @@
 A single-source field runs on one GPU.  Batched workloads (distance-matrix
 rows, farthest-point sampling rounds) split their sources over the ranks
 of one node -- one process per GPU, each holding a replica of the mesh
-(``device_mesh``) -- and the rows are gathered once at the end (NCCL over
-NVLink on the GPUs, gloo on CPU in the tests).  There is no data-path
-collective: ranks never exchange windows or partial fields.
+(``device_mesh``) -- and the rows are gathered once at the end onto rank 0
+(NCCL over NVLink on the GPUs, device memory to device memory; gloo on CPU
+in the tests).  There is no data-path collective: ranks never exchange
+windows or partial fields.
 
 Reference context: the reference computes multi-source fields and
 repeated single-source runs on one host (engine.py:433, cli.py:103,
@@ -25,35 +26,43 @@ def shard_sources(sources, rank: int, world: int) -> np.ndarray:
     return np.arange(rank, n, world, dtype=np.int64)
 
 
-def gather_rows(local_rows: np.ndarray, n_total: int, rank: int, world: int,
-                device=None) -> np.ndarray | None:
-    """Collect every rank's rows (``shard_sources`` order) into the
-    original source order on all ranks.  ``local_rows`` is
-    ``[len(shard), n_vertices]`` float64."""
+def gather_rows(local, n_total: int, rank: int, world: int):
+    """Collect every rank's rows (``shard_sources`` order) onto rank 0 in
+    the original source order.  ``local`` is a ``[len(shard), n_vertices]``
+    float64 torch tensor on this rank's device (NCCL) or on the CPU (gloo);
+    rank 0 returns the ``[n_total, n_vertices]`` tensor on the same device,
+    the other ranks ``None``.  One collective, no host round trip."""
     import torch
     import torch.distributed as dist
 
-    nv = local_rows.shape[1] if local_rows.ndim == 2 else 0
+    nv = int(local.shape[1])
     counts = [len(shard_sources(range(n_total), r, world)) for r in range(world)]
-    cmax = max(counts) if counts else 0
-    dev = device if device is not None else torch.device("cpu")
-    buf = torch.full((cmax, nv), float("nan"), dtype=torch.float64, device=dev)
-    if len(local_rows):
-        buf[: len(local_rows)] = torch.as_tensor(local_rows, dtype=torch.float64, device=dev)
-    outs = [torch.empty_like(buf) for _ in range(world)]
-    dist.all_gather(outs, buf)
-    rows = np.empty((n_total, nv), dtype=np.float64)
+    cmax = max(counts)
+    if local.shape[0] < cmax:  # equal-size buffers for the collective
+        pad = torch.full((cmax - local.shape[0], nv), float("nan"), dtype=local.dtype,
+                         device=local.device)
+        local = torch.cat([local, pad])
+    bufs = [torch.empty_like(local) for _ in range(world)] if rank == 0 else None
+    dist.gather(local.contiguous(), bufs, dst=0)
+    if rank != 0:
+        return None
+    out = torch.empty((n_total, nv), dtype=local.dtype, device=local.device)
     for r in range(world):
-        idx = shard_sources(range(n_total), r, world)
-        rows[idx] = outs[r][: counts[r]].cpu().numpy()
-    return rows
+        idx = torch.as_tensor(shard_sources(range(n_total), r, world), device=local.device)
+        if len(idx):
+            out.index_copy_(0, idx, bufs[r][: counts[r]])
+    return out
 
 
-def run_rows_sharded(mesh, sources, config=None, solve=None, device=None):
+def run_rows_sharded(mesh, sources, config=None, solve=None):
     """Distance-matrix rows for ``sources`` computed by all ranks of the
-    initialised process group; every rank returns the full
-    ``[len(sources), n_vertices]`` array.  ``solve(mesh, sources, config)``
-    defaults to the GPU ``run_pch_rows`` on this rank's device."""
+    initialised process group (or this process alone); rank 0 returns the
+    full ``[len(sources), n_vertices]`` float64 numpy array, the other
+    ranks ``None``.  The default ``solve`` is the GPU path: this rank's
+    share through ``run_pch_rows_device`` into device memory, gathered over
+    NCCL device to device; ``solve(mesh, sources, config) -> array`` (the
+    CPU tests' oracle) is gathered over gloo."""
+    import torch
     import torch.distributed as dist
 
     world = dist.get_world_size() if dist.is_initialized() else 1
@@ -61,9 +70,18 @@ def run_rows_sharded(mesh, sources, config=None, solve=None, device=None):
     src = np.asarray([int(s) for s in sources], dtype=np.int64)
     mine = src[shard_sources(src, rank, world)]
     if solve is None:
-        from .engine import run_pch_rows
-        solve = lambda m, s, c: run_pch_rows(m, s, c)[0]  # noqa: E731
-    local = solve(mesh, mine, config) if len(mine) else np.empty((0, mesh.n_vertices))
+        from .engine import EngineConfig, run_pch_rows_device
+        config = config or EngineConfig()
+        dev = torch.device("cuda", config.device)
+        local = torch.empty((len(mine), mesh.n_vertices), dtype=torch.float64, device=dev)
+        if len(mine):
+            d_src = torch.as_tensor(mine, device=dev)
+            run_pch_rows_device(mesh, d_src.data_ptr(), len(mine), local.data_ptr(), config,
+                                stream=torch.cuda.current_stream(dev).cuda_stream)
+    else:
+        rows = solve(mesh, mine, config) if len(mine) else np.empty((0, mesh.n_vertices))
+        local = torch.as_tensor(np.asarray(rows, dtype=np.float64))
     if world == 1:
-        return np.asarray(local)
-    return gather_rows(np.asarray(local), len(src), rank, world, device)
+        return local.cpu().numpy()
+    out = gather_rows(local, len(src), rank, world)
+    return None if out is None else out.cpu().numpy()

@@ -93,6 +93,7 @@ struct Params {
     const FanRec *fan;
     const FanHdr *fanhdr;      // [nv] wedge range, total angle, interior flag
     const double *anchor_wlo;  // [nhe] start angle of h's wedge in origin(h)'s fan
+    const double2 *apex_xy;    // [nhe] apex of face(h) unfolded in the frame of edge h (geom.py:390-396)
     int32_t nv, nhe;
     // distance field / angle-split table: frozen + shadow copies
     double *dist_cur;
@@ -379,6 +380,7 @@ constexpr int FAN_LANES = 8;      // lanes per saddle fan (wedges x repetitions)
 constexpr int FANS_PER_WARP = 32 / FAN_LANES;
 
 constexpr int FE_CAP = 2 * TPB;
+
 
 
 struct Stage {
@@ -711,6 +713,9 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const double ell = __ldg(&fp->len[a]);
     const double lan = __ldg(&fp->len[a1]);
     const double lpv = __ldg(&fp->len[a2]);
+    // the far triangle's apex D below the edge, precomputed per half-edge
+    // (geom.py:387-396), loaded with the face record
+    const double2 dxy = __ldg(p.apex_xy + fr);
     // the window's vertices (carried from its creation): the distances
     // below are issued together with the face record
     const uint32_t v0f = w.v0f, v1f = w.v1f, vdf = far ? w.vdf : 0u;
@@ -749,9 +754,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const bool ev1 = !rechecked && b1 >= ell - p.eps_win && cand1 < g1;
 
     // the far triangle: apex D below the edge (geom.py:387-516)
-    const double dx = 0.5 * (ell * ell + lan * lan - lpv * lpv) / ell;
-    const double dy2 = lan * lan - dx * dx;
-    const double dy = dy2 > 0.0 ? -sqrt(dy2) : 0.0;
+    const double dx = dxy.x, dy = dxy.y;
     const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
     const double vdx = dx - ix, vdy = dy - iy;
     const double nvd2 = vdx * vdx + vdy * vdy;
@@ -972,6 +975,9 @@ __device__ __forceinline__ void flush_hist(unsigned int *s_hist, unsigned int *g
 
 #ifndef PCH_MIN_BLOCKS
 #define PCH_MIN_BLOCKS 1  // resident CTAs per SM the register budget targets
+#endif
+#ifndef PCH_LIVE_MIN_BLOCKS
+#define PCH_LIVE_MIN_BLOCKS 1  // ... of the one-barrier solver
 #endif
 
 __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) {
@@ -1295,7 +1301,7 @@ __device__ __forceinline__ void warp_chunk_alloc2(unsigned long long *s_cnt, uns
 // request only (EngineConfig.phase_times): the clock reads and per-item
 // shared adds on the batch warps' critical path cost ~3 % of a field
 template <bool PHASE>
-__global__ void __launch_bounds__(TPB, 1) pch_live(Params p) {
+__global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     // Outputs are chunked per CTA: CTA b writes the windows it routes to
     // slots [b*ch, (b+1)*ch) of the next batch / pool and its fan
     // candidates to [b*chF, (b+1)*chF), allocating with one shared atomic
@@ -1777,6 +1783,7 @@ struct pch_mesh {
     FanRec *fan = nullptr;
     FanHdr *fanhdr = nullptr;
     double *anchor_wlo = nullptr;
+    double2 *apex_xy = nullptr;
     size_t mesh_bytes = 0;
     // workspace
     long long cap = 0;
@@ -1847,6 +1854,7 @@ static int ensure_ws(pch_mesh *m, long long cap, int rows) {
     p.fan = m->fan;
     p.fanhdr = m->fanhdr;
     p.anchor_wlo = m->anchor_wlo;
+    p.apex_xy = m->apex_xy;
     p.nv = m->nv;
     p.nhe = m->nhe;
     if ((rc = ws_alloc(m, &p.dist_cur, m->nv))) return rc;
@@ -2275,6 +2283,18 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
         awlo[j] = fan[fan_off[v] + fanpos[j]].wlo;
     }
 
+    // precomputed unfolding: the apex of face(h) in the frame of edge h
+    // (origin(h) at 0, dest(h) at (|h|, 0), apex below the edge) -- the far
+    // triangle of every window on opposite(h) (geom.py:390-396), computed
+    // once instead of a division and a square root per crossing
+    std::vector<double2> apex(nhe);
+    for (int64_t h = 0; h < nhe; ++h) {
+        const double ell = length[h], lan = length[nxt_he(h)], lpv = length[prv_he(h)];
+        const double dx = 0.5 * (ell * ell + lan * lan - lpv * lpv) / ell;
+        const double dy2 = lan * lan - dx * dx;
+        apex[h] = make_double2(dx, dy2 > 0.0 ? -std::sqrt(dy2) : 0.0);
+    }
+
     pch_mesh *m = new pch_mesh();
     m->device = device;
     m->nv = (int32_t)n_vertices;
@@ -2306,7 +2326,8 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
     if ((e = up((void **)&m->face, face.data(), sizeof(FaceRec) * n_faces)) != cudaSuccess ||
         (e = up((void **)&m->fan, fan.data(), sizeof(FanRec) * fan.size())) != cudaSuccess ||
         (e = up((void **)&m->fanhdr, hdr.data(), sizeof(FanHdr) * n_vertices)) != cudaSuccess ||
-        (e = up((void **)&m->anchor_wlo, awlo.data(), sizeof(double) * nhe)) != cudaSuccess)
+        (e = up((void **)&m->anchor_wlo, awlo.data(), sizeof(double) * nhe)) != cudaSuccess ||
+        (e = up((void **)&m->apex_xy, apex.data(), sizeof(double2) * nhe)) != cudaSuccess)
         return cleanup(PCH_ERR_CUDA, std::string("mesh upload: ") + cudaGetErrorString(e));
     if ((e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking)) != cudaSuccess ||
         (e = cudaEventCreate(&m->ev0)) != cudaSuccess || (e = cudaEventCreate(&m->ev1)) != cudaSuccess ||
@@ -2334,6 +2355,7 @@ int pch_mesh_destroy(pch_mesh *m) {
     cudaFree(m->fan);
     cudaFree(m->fanhdr);
     cudaFree(m->anchor_wlo);
+    cudaFree(m->apex_xy);
     cudaFree(m->d_src);
     cudaFree(m->fps_buf);
     cudaFree(m->d_out);

@@ -21,11 +21,21 @@ name = os.environ["WL"]
 m = M.bench_mesh(name)
 src = 354 * 709 + 354 if name == "terrain1m" else int(np.argmin(np.linalg.norm(m.positions - m.positions.mean(0), axis=1)))
 kw = json.loads(os.environ.get("CFG", "{}"))
+nrows = int(kw.pop("rows", 0))
 cfg = EngineConfig(**kw)
-for _ in range(3):
+if nrows:
+    from paper_1305_1293_b200 import run_pch_rows
+    srcs = np.random.default_rng(4096).choice(m.n_vertices, nrows, replace=False)
+    run_pch_rows(m, srcs[:32], cfg)
+    ts = []
+    for _ in range(int(os.environ.get("N", "2"))):
+        rows, st = run_pch_rows(m, srcs, cfg)
+        ts.append(st.time_kernel_ms / nrows)  # ms per row
+else:
+  for _ in range(3):
     run_pch(m, [src], cfg)
-ts = []
-for _ in range(int(os.environ.get("N", "5"))):
+  ts = []
+  for _ in range(int(os.environ.get("N", "5"))):
     d, st = run_pch(m, [src], cfg)
     ts.append(st.time_kernel_ms)
 print(json.dumps({"ms": ts, "iters": st.iterations, "created": st.total_windows_created}))

@@ -9,6 +9,7 @@
  * No torch types, no C++ types: every argument is a pointer + size.
  *
  * Entry points and the reference interface each one replaces:
+ *   pch_half_edge_build  build_half_edge_mesh(positions, faces) (mesh.py:142)
  *   pch_mesh_create   build_half_edge_mesh result -> device-resident mesh
  *                     (mesh.py:142 output; the paper's §4.1 `he[]`,
  *                      `outgoing_he[]` plus precomputed unfoldings)
@@ -137,6 +138,27 @@ typedef struct pch_stats {
 } pch_stats;
 
 typedef struct pch_mesh pch_mesh;
+
+/* Half-edge construction on the host (reference mesh.py:142
+ * build_half_edge_mesh): positions double[n_vertices * 3], faces
+ * int64[n_faces * 3] (consistently oriented) in; the SurfaceMesh arrays
+ * out -- origin / opposite (-1 on a boundary) / length / corner_angle
+ * [3 n_faces], total_angle / vertex_class (0 spherical, 1 euclidean,
+ * 2 saddle) / outgoing / on_boundary [n_vertices].  Lengths are
+ * bit-identical to the reference's numpy arithmetic; with corner_cos_only
+ * the corner_angle array receives the clipped law-of-cosines ratio and
+ * total_angle / vertex_class are left to the caller (numpy's arccos and the
+ * C library's differ in the last bit; the Python layer applies numpy's).
+ * Returns PCH_ERR_MESH with the reference's MeshError message in
+ * pch_half_edge_error() for bad indices, repeated vertices, zero-length
+ * edges, degenerate triangles, non-manifold edges or vertices.  No GPU. */
+int pch_half_edge_build(const double *positions, int64_t n_vertices,
+                        const int64_t *faces, int64_t n_faces,
+                        int64_t *origin, int64_t *opposite, double *length,
+                        double *corner_angle, double *total_angle,
+                        uint8_t *vertex_class, int64_t *outgoing,
+                        uint8_t *on_boundary, int32_t corner_cos_only);
+const char *pch_half_edge_error(void);
 
 /* Library identity. */
 int pch_abi_version(void);

@@ -63,7 +63,7 @@ class PchStats(ctypes.Structure):
 EXPORTS = ("pch_abi_version", "pch_last_error", "pch_device_count",
            "pch_mesh_create", "pch_mesh_destroy", "pch_mesh_device_bytes",
            "pch_run", "pch_run_device", "pch_run_rows", "pch_run_rows_device",
-           "pch_fps", "pch_probe")
+           "pch_fps", "pch_probe", "pch_half_edge_build", "pch_half_edge_error")
 
 _lib = None
 
@@ -106,6 +106,9 @@ def load():
     lib.pch_fps.restype = ctypes.c_int
     lib.pch_probe.argtypes = [ctypes.c_int32, P, ctypes.c_int32]
     lib.pch_probe.restype = ctypes.c_int
+    lib.pch_half_edge_build.argtypes = [P, i64, P, i64, P, P, P, P, P, P, P, P, ctypes.c_int32]
+    lib.pch_half_edge_build.restype = ctypes.c_int
+    lib.pch_half_edge_error.restype = ctypes.c_char_p
     if lib.pch_abi_version() != ABI_VERSION:
         raise NativeUnavailable("libpch_b200.so ABI version mismatch")
     _lib = lib

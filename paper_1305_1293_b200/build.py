@@ -11,12 +11,12 @@ ROOT = os.path.dirname(_HERE)
 CSRC = os.path.join(_HERE, "csrc")
 OUT = os.path.join(_HERE, "_lib", "libpch_b200.so")
 
-SOURCES = ["pch_engine.cu"]
+SOURCES = ["pch_engine.cu", "pch_mesh.cpp"]
 DEPS = ["pch_device.cuh", os.path.join(ROOT, "include", "pch_b200.h")]
 
 NVCC_FLAGS = ["-std=c++17", "-O3", "-lineinfo",
               "-gencode", "arch=compute_100a,code=sm_100a",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC,-ffp-contract=off", "-shared", "-Xptxas", "-v"]
 
 
 def _nvcc() -> str:

@@ -40,7 +40,7 @@ def golden_cases():
     """Reference-generated fixtures (make_golden.py); the large_* oracle
     fixtures of the configuration meshes (make_large.py) are separate."""
     return sorted(os.path.basename(p)[:-4] for p in glob.glob(os.path.join(GOLDEN, "*.npz"))
-                  if not os.path.basename(p).startswith("large_"))
+                  if not os.path.basename(p).startswith(("large_", "mesh_arrays")))
 
 
 def load_golden(name):

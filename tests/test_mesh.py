@@ -107,3 +107,18 @@ def test_build_matches_reference_arithmetic_bitwise():
     p, f = g["positions"], g["faces"]
     vec = p[np.roll(f, -1, axis=1).reshape(-1)] - p[f.reshape(-1)]
     assert np.array_equal(m.length, np.sqrt(np.sum(vec * vec, axis=1)))
+
+
+def test_native_builder_bitwise_matches_reference():
+    """The native construction (pch_half_edge_build) reproduces the
+    reference's SurfaceMesh arrays bit for bit (fixtures made by the
+    reference itself, tests/golden/make_mesh_golden.py)."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "mesh_arrays.npz"))
+    names = sorted({k.split("/")[0] for k in g.files})
+    assert names
+    for name in names:
+        m = build_half_edge_mesh(g[f"{name}/positions"], g[f"{name}/faces"])
+        for k in ("origin", "opposite", "length", "corner_angle", "total_angle", "vertex_class",
+                  "outgoing", "on_boundary"):
+            assert np.array_equal(getattr(m, k), g[f"{name}/{k}"]), (name, k)

@@ -118,7 +118,10 @@ typedef struct pch_stats {
     int64_t events_applied;
     int64_t peak_active_pool;
     int64_t fans_emitted;
-    int64_t buffer_regrows;
+    int64_t buffer_regrows;   /* window-pool growths (RunStats.buffer_regrows) */
+    int64_t pool_restarts;    /* ... of which reran the solve from scratch (a
+                                 hard overflow); the live solver grows at an
+                                 iteration boundary and continues */
     double time_total_ms;     /* device time of the solve (CUDA events) */
     double time_kernel_ms;    /* persistent-kernel time only */
     /* RunStats.time_select / _propagate / _compact / _events

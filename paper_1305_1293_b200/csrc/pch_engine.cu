@@ -84,7 +84,9 @@ struct Ctrl {
     unsigned long long st[N_ST];
     double t_final;
     int final_parity;  // which of X/Y held the last pool (unused on exit)
-    int pad1;
+    int grow;          // live solver: a chunk passed its soft limit -> stop at the iteration end, grow, resume
+    long long res_it;  // ... the iteration to resume at, its threshold and controller step
+    double res_t, res_delta;
 };
 
 struct Params {
@@ -117,6 +119,7 @@ struct Params {
     double inv_r0;             // 1 / radius of the angular tiny-window rule (huge: absolute)
     double fan_widen;          // saddle-fan interval widened by this angle on both sides
     int phase;                 // attribute cycles to the four phases (PCH_FLAG_PHASE_TIMES)
+    int resume;                // live solver: continue at ctrl->res_it after a pool growth
     double w0;
     double delta0, delta_min, delta_max;  // one-barrier step controller
     long long max_iter;
@@ -374,6 +377,10 @@ constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more c
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;
+#ifndef PCH_POOL_MIN
+#define PCH_POOL_MIN (1ll << 21)
+#endif
+constexpr long long DEFAULT_POOL_MIN = PCH_POOL_MIN;  // first window-pool capacity (at least)
 constexpr double TINY_R0_EDGES = 40.0;  // angular tiny-window radius, mean edge lengths      // fields pch_run_rows solves together (at most)
 constexpr int MAX_CTAS = 1024;        // chunk-count tables of the live solver
 constexpr int FAN_LANES = 8;      // lanes per saddle fan (wedges x repetitions)
@@ -1318,7 +1325,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     __shared__ unsigned long long s_nsp;        // this CTA's outputs: S (low) / P (high)
     __shared__ unsigned int s_nf;               // this CTA's fan candidates
     __shared__ unsigned long long s_pmin, s_smax;
-    __shared__ unsigned long long s_c[3];       // err, pmin, smax of the finished iteration
+    __shared__ unsigned long long s_c[4];       // err, pmin, smax, grow of the finished iteration
     stats_init(s_st);
     if (threadIdx.x == 0) {
         sg.ntv = sg.nte = sg.nfe = 0u;
@@ -1337,8 +1344,11 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     const unsigned long long gwid = (unsigned long long)(threadIdx.x >> 5) * G + b;
     const int lane = threadIdx.x & 31;
     const unsigned long long t_start = globaltimer();
-    double t = 0.0;           // threshold S_i was selected with
-    double delta = p.delta0;  // controller step
+    // a resumed launch (pool grown at an iteration boundary) continues with
+    // the saved iteration, threshold and step; its inputs were migrated
+    // into the enlarged chunks by k_migrate_chunks
+    double t = p.resume ? ctrl->res_t : 0.0;           // threshold S_i was selected with
+    double delta = p.resume ? ctrl->res_delta : p.delta0;  // controller step
     // prefix tables of the iteration's inputs from the per-CTA counts
     // (and, with `slot`, the controller's inputs in the same round trip)
     auto build_prefix = [&](int par_in, int par_fan, const Slot *slot) {
@@ -1346,6 +1356,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             s_c[0] = (unsigned long long)__ldcg(&ctrl->error);
             s_c[1] = __ldcg(&slot->pmin);
             s_c[2] = __ldcg(&slot->smax);
+            s_c[3] = (unsigned long long)__ldcg(&ctrl->grow);
         }
         if (threadIdx.x < 96) {
             const int q = threadIdx.x >> 5;  // 0: S, 1: P, 2: fans of the previous iteration
@@ -1378,8 +1389,10 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         }
         __syncthreads();
     };
-    build_prefix(0, 1, &ctrl->slot[0]);  // S_0: the source windows (chunk-published by k_source_windows)
-    int it = 0;
+    int it = p.resume ? (int)ctrl->res_it : 0;
+    // S_0: the source windows (chunk-published by k_source_windows), or the
+    // inputs of the resumed iteration
+    build_prefix(it & 1, (it & 1) ^ 1, &ctrl->slot[it % NSLOT]);
     // an initialisation failure (a source-window chunk overflowed, an
     // invalid device source) makes the published counts meaningless: every
     // CTA read the same flag with the prefix tables and skips the loop
@@ -1625,6 +1638,14 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             p.ccnt[(size_t)(po * 3 + 0) * MAX_CTAS + b] = min((unsigned int)s_nsp, (unsigned int)ch);
             p.ccnt[(size_t)(po * 3 + 1) * MAX_CTAS + b] = min((unsigned int)(s_nsp >> 32), (unsigned int)ch);
             p.ccnt[(size_t)(par * 3 + 2) * MAX_CTAS + b] = min(s_nf, (unsigned int)chF);
+            // past half a chunk: finish this iteration, then grow the pool
+            // and resume (host), instead of overflowing in a later one (a
+            // CTA adds well under half a chunk per iteration)
+            const unsigned long long soft = ch / 2, softF = chF / 2;
+#ifndef PCH_NO_SOFT
+            if ((s_nsp & 0xffffffffull) > soft || (s_nsp >> 32) > soft || s_nf > softF)
+                atomicExch(&ctrl->grow, 1);
+#endif
             s_nsp = 0ull;
             s_nf = 0u;
             if (s_pmin != ~0ull) atomicMin(&nxt.pmin, s_pmin);
@@ -1654,6 +1675,16 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         ++it;
         if (err || (ns == 0 && np == 0 && nf == 0)) break;
         t = tn;
+        if (s_c[3]) {
+            // grow request: every CTA saw it with the counts; the inputs of
+            // iteration `it` are complete in their chunks
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                ctrl->res_it = it;
+                ctrl->res_t = t;
+                ctrl->res_delta = delta;
+            }
+            break;
+        }
     }
     __syncwarp();
     ls.fold();
@@ -1746,6 +1777,26 @@ __global__ void k_source_windows(Params p, const int64_t *src, int nsrc) {
         }
     }
     flush_stats(ctrl, s_st);
+}
+
+// Pool growth without a restart (live solver): the inputs of the resumed
+// iteration -- batch S, pool P (both parity `par`) and the fan candidates
+// of the previous iteration (parity par^1) -- move from their chunks of
+// the old capacity (ch, chF per CTA) to the same chunks of the new one.
+__global__ void k_migrate_chunks(WinSoA S_old, WinSoA P_old, const FanEv *F_old, WinSoA S_new, WinSoA P_new,
+                                 FanEv *F_new, const unsigned int *ccnt, int par, int G,
+                                 unsigned long long ch_old, unsigned long long ch_new,
+                                 unsigned long long chF_old, unsigned long long chF_new) {
+    const int b = blockIdx.y;  // chunk
+    const unsigned int nS = ccnt[(size_t)(par * 3 + 0) * MAX_CTAS + b];
+    const unsigned int nP = ccnt[(size_t)(par * 3 + 1) * MAX_CTAS + b];
+    const unsigned int nF = ccnt[(size_t)((par ^ 1) * 3 + 2) * MAX_CTAS + b];
+    for (unsigned int i = blockIdx.x * blockDim.x + threadIdx.x; i < max(max(nS, nP), nF);
+         i += gridDim.x * blockDim.x) {
+        if (i < nS) store_win(S_new, b * ch_new + i, load_win(S_old, b * ch_old + i));
+        if (i < nP) store_win(P_new, b * ch_new + i, load_win(P_old, b * ch_old + i));
+        if (i < nF) F_new[b * chF_new + i] = F_old[b * chF_old + i];
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1842,9 +1893,11 @@ static int alloc_soa(pch_mesh *m, WinSoA &W, long long cap) {
     return PCH_OK;
 }
 
-static int ensure_ws(pch_mesh *m, long long cap, int rows) {
-    if (m->cap >= cap && m->rows_alloc >= rows) return PCH_OK;
-    cap = std::max(cap, m->cap);
+// `exact`: an explicit pool capacity (EngineConfig.pool_capacity) is
+// honoured even when the mesh's workspace is larger
+static int ensure_ws(pch_mesh *m, long long cap, int rows, bool exact = false) {
+    if ((exact ? m->cap == cap : m->cap >= cap) && m->rows_alloc >= rows) return PCH_OK;
+    if (!exact) cap = std::max(cap, m->cap);
     rows = std::max(rows, m->rows_alloc);
     free_ws(m);
     Params &p = m->prm;
@@ -1888,6 +1941,48 @@ static int ensure_ws(pch_mesh *m, long long cap, int rows) {
     return PCH_OK;
 }
 
+// Enlarge the cap-sized buffers (window SoAs, fan candidates, event lists)
+// to `cap`, moving the resumed iteration's inputs (parity `par`) chunk by
+// chunk; the distance / angle-split / pick tables and the counters stay.
+static int grow_ws(pch_mesh *m, long long cap, int par, cudaStream_t st) {
+    Params &p = m->prm;
+    const int G = m->grid_live;
+    const long long old_cap = p.cap, old_fancap = p.fancap;
+    std::vector<void *> old = {p.X.hv, p.X.vr, p.X.b0, p.X.b1, p.X.d0, p.X.d1, p.X.d, p.X.key,
+                               p.Y.hv, p.Y.vr, p.Y.b0, p.Y.b1, p.Y.d0, p.Y.d1, p.Y.d, p.Y.key,
+                               p.S.hv, p.S.vr, p.S.b0, p.S.b1, p.S.d0, p.S.d1, p.S.d, p.S.key,
+                               p.S2.hv, p.S2.vr, p.S2.b0, p.S2.b1, p.S2.d0, p.S2.d1, p.S2.d, p.S2.key,
+                               p.fanev[0], p.fanev[1], p.fanev[2], p.tv_list, p.te_list};
+    const WinSoA oX = p.X, oY = p.Y, oS = p.S, oS2 = p.S2;
+    FanEv *oF[3] = {p.fanev[0], p.fanev[1], p.fanev[2]};
+    int rc;
+    if ((rc = alloc_soa(m, p.X, cap)) || (rc = alloc_soa(m, p.Y, cap)) || (rc = alloc_soa(m, p.S, cap)) ||
+        (rc = alloc_soa(m, p.S2, cap)))
+        return rc;
+    p.fancap = std::max<long long>(cap, 1 << 16);
+    for (int q = 0; q < 3; ++q)
+        if ((rc = ws_alloc(m, &p.fanev[q], p.fancap))) return rc;
+    p.tvcap = 3 * cap + m->nv;
+    p.tecap = cap + m->nhe;
+    if ((rc = ws_alloc(m, &p.tv_list, p.tvcap)) || (rc = ws_alloc(m, &p.te_list, p.tecap))) return rc;
+    const unsigned long long ch_old = old_cap / G, ch_new = cap / G;
+    const unsigned long long chF_old = old_fancap / G, chF_new = p.fancap / G;
+    k_migrate_chunks<<<dim3(64, G), 256, 0, st>>>(par ? oS2 : oS, par ? oY : oX, oF[par ^ 1], par ? p.S2 : p.S,
+                                                  par ? p.Y : p.X, p.fanev[par ^ 1], p.ccnt, par, G, ch_old,
+                                                  ch_new, chF_old, chF_new);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    for (void *q : old) {
+        cudaFree(q);
+        m->ws.erase(std::remove(m->ws.begin(), m->ws.end(), q), m->ws.end());
+    }
+    m->ws_bytes -= (size_t)old_cap * 4 * 72 + (size_t)old_fancap * 3 * sizeof(FanEv) +
+                   sizeof(int32_t) * ((size_t)(3 * old_cap + m->nv) + (size_t)(old_cap + m->nhe));
+    p.cap = cap;
+    m->cap = cap;
+    return PCH_OK;
+}
+
 // rows == 1: one field from the union of the sources (reference run_pch);
 // rows == nsrc > 1: one field per source, solved together (batched rows,
 // live solver only)
@@ -1901,16 +1996,22 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
     if (rows > 1 && (cfg->flags & PCH_FLAG_DETERMINISTIC))
         return fail(PCH_ERR_CONFIG, "batched rows need the live solver");
     // the pool holds every row's wavefront: scale the first guess with rows
+    // the live solver grows its pool at an iteration boundary and continues
+    // (grow_ws), so the first capacity only needs to cover the early
+    // wavefront: a quarter window per half-edge (peak active pools measured
+    // 0.4M windows on the 16M-face sphere, 3M for 32 torus rows)
     long long cap = cfg->pool_capacity > 0
                         ? cfg->pool_capacity
-                        : std::max<long long>(1 << 20, 2ll * m->nhe) * std::max(1, rows / 4);
-    if (m->cap > cap) cap = m->cap;
+                        : std::max<long long>(DEFAULT_POOL_MIN, m->nhe / 4) * std::max(1, rows / 4);
+    if (cfg->pool_capacity <= 0 && m->cap > cap) cap = m->cap;
     // every per-CTA chunk of the live solver holds at least 8 windows
     cap = std::max<long long>(cap, 8ll * m->grid_live);
-    int regrows = 0;
+    bool exact = cfg->pool_capacity > 0;
+    int regrows = 0, restarts = 0;
     for (;;) {
-        int rc = ensure_ws(m, cap, rows);
+        int rc = ensure_ws(m, cap, rows, exact);
         if (rc) return rc;
+        exact = false;  // a rerun after a hard overflow only grows
         Params p = m->prm;
         p.seed = d_seed;
         p.K = cfg->k;
@@ -2000,10 +2101,43 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         CK(cudaStreamSynchronize(st));
         Ctrl c;
         CK(cudaMemcpy(&c, p.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+        // a chunk passed its soft limit: the live solver stopped at an
+        // iteration boundary with every window in place -- grow the pool,
+        // move the next iteration's inputs, continue where it stopped
+        while (p.live && c.error == ERR_NONE && c.grow) {
+            if (cap >= (1ll << 31)) return fail(PCH_ERR_NOMEM, "window pool at maximum capacity");
+            int rc2 = grow_ws(m, cap * 2, (int)(c.res_it & 1), st);
+            if (rc2) return rc2;
+            cap *= 2;
+            regrows++;
+            p.X = m->prm.X;
+            p.Y = m->prm.Y;
+            p.S = m->prm.S;
+            p.S2 = m->prm.S2;
+            for (int q = 0; q < 3; ++q) p.fanev[q] = m->prm.fanev[q];
+            p.fancap = m->prm.fancap;
+            p.tv_list = m->prm.tv_list;
+            p.te_list = m->prm.te_list;
+            p.tvcap = m->prm.tvcap;
+            p.tecap = m->prm.tecap;
+            p.cap = cap;
+            p.resume = 1;
+            CK(cudaMemsetAsync(&p.ctrl->grow, 0, sizeof(int), st));
+            CK(cudaMemsetAsync(&p.ctrl->bar_count, 0, sizeof(unsigned int), st));
+            void *args2[] = {&p};
+            const void *kern = p.phase ? (const void *)pch_live<true> : (const void *)pch_live<false>;
+            CK(cudaLaunchCooperativeKernel(kern, dim3(p.live_grid), dim3(TPB), args2, 0, st));
+            CK(cudaEventRecord(m->ev2, st));
+            CK(cudaStreamSynchronize(st));
+            CK(cudaMemcpy(&c, p.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+        }
         if (c.error == ERR_OVERFLOW) {
+            // hard overflow (a chunk filled within one iteration, the
+            // source windows, or the two-barrier solver): rerun at 2x
             if (cap >= (1ll << 31)) return fail(PCH_ERR_NOMEM, "window pool overflow at maximum capacity");
             cap *= 2;
             regrows++;
+            restarts++;
             continue;
         }
         if (p.trace) {
@@ -2061,6 +2195,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             stats->peak_active_pool = std::max<int64_t>(stats->peak_active_pool, c.st[ST_PEAK]);
             stats->fans_emitted += c.st[ST_FANS];
             stats->buffer_regrows += regrows;
+            stats->pool_restarts += restarts;
             stats->time_total_ms += t_all;
             stats->time_kernel_ms += t_k;
             // phase shares of the kernel time from the warp-cycle attribution
@@ -2475,7 +2610,7 @@ static int run_rows(pch_mesh *m, const int64_t *d_sources, int64_t n_sources, co
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
             const double budget = 0.5 * (double)(free_b + m->ws_bytes);
             const double per_row = 24.0 * m->nv + 16.0 * m->nhe;
-            const double base = (double)std::max<long long>(1 << 20, 2ll * m->nhe);
+            const double base = (double)std::max<long long>(DEFAULT_POOL_MIN, m->nhe / 4);
             auto est = [&](int r) { return r * per_row + base * std::max(1, r / 4) * 472.0; };
             while (R > 1 && est(R) > budget) R /= 2;
         }

@@ -151,6 +151,7 @@ class RunStats:
     peak_active_pool: int = 0
     fans_emitted: int = 0
     buffer_regrows: int = 0
+    pool_restarts: int = 0
     time_total: float = 0.0
     time_select: float = 0.0
     time_propagate: float = 0.0

@@ -160,3 +160,19 @@ def test_config_rows_torus500k():
         assert np.array_equal(np.isfinite(single), np.isfinite(rows[r]))
         both = np.isfinite(single)
         assert np.max(np.abs(single[both] - rows[r][both]) / np.maximum(single[both], 1e-12)) <= TOL
+
+
+def test_sphere16m_rows_grow_without_rerun():
+    """configs[3] mesh, batched rows from a deliberately small pool: the
+    pool grows at iteration boundaries (windows migrated, solve resumed),
+    never rerun, and the rows match single-source fields."""
+    from paper_1305_1293_b200 import EngineConfig, run_pch, run_pch_rows
+    m, g = _fixture("sphere16m")
+    src = [int(g["source"]), 17, 4_000_000]
+    rows, st = run_pch_rows(m, src, EngineConfig(pool_capacity=1 << 19))
+    assert st.buffer_regrows >= 1 and st.pool_restarts == 0
+    check_field(m, rows[0], g, "sphere16m row 0")
+    one, _ = run_pch(m, [src[2]])
+    assert np.array_equal(np.isfinite(one), np.isfinite(rows[2]))
+    fin = np.isfinite(one)
+    assert np.max(np.abs(rows[2][fin] - one[fin]) / np.maximum(one[fin], 1e-12)) <= TOL

@@ -168,12 +168,22 @@ def test_iteration_guard_raises():
 
 
 def test_small_pool_regrows():
+    """A pool that starts far too small grows at iteration boundaries and
+    the solve continues (no rerun): the iteration count equals the one of a
+    run that never grew, give or take the grown run's step decisions."""
     _gpu()
     from paper_1305_1293_b200 import EngineConfig, run_pch
     m, g = load_golden("icosphere20480_s1370")
     d, st = run_pch(m, g["sources"], EngineConfig(pool_capacity=256))
     assert st.buffer_regrows >= 1
     assert max_rel_dev(d, g["ich_dist"]) <= TOL
+    _, ref = run_pch(m, g["sources"], EngineConfig())
+    assert ref.buffer_regrows == 0
+    assert st.iterations <= ref.iterations + 4 * st.buffer_regrows
+    # a moderately small pool grows without ever rerunning the solve
+    d2, st2 = run_pch(m, g["sources"], EngineConfig(pool_capacity=1 << 14))
+    assert st2.buffer_regrows >= 1 and st2.pool_restarts == 0
+    assert max_rel_dev(d2, g["ich_dist"]) <= TOL
 
 
 def test_edge_lipschitz_and_sandwich_terrain():

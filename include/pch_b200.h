@@ -89,6 +89,11 @@ typedef struct pch_config {
 #define PCH_FLAG_PHASE_TIMES 8  /* fill pch_stats.time_select/_propagate/
                                      _compact/_events_ms and prop_item_us
                                      (warp-cycle attribution, ~3 % slower) */
+#define PCH_FLAG_DEDUPE 16  /* drop exact-duplicate fan windows as the
+                                reference does (engine.py:201), counted in
+                                pruned_duplicate; off by default: the
+                                per-vertex fan pick leaves ~0.02 % twins
+                                and the fingerprint table costs ~10 % */
 #define PCH_FLAG_ABSOLUTE_TINY 4  /* the reference's absolute tiny-window
                                      drop (width <= epsilon_window,
                                      geom.py:133) everywhere; default: the

@@ -26,6 +26,7 @@ FLAG_NO_RECHECK = 1
 FLAG_DETERMINISTIC = 2
 FLAG_ABSOLUTE_TINY = 4
 FLAG_PHASE_TIMES = 8
+FLAG_DEDUPE = 16
 
 
 class NativeUnavailable(RuntimeError):

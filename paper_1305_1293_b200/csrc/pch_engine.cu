@@ -50,7 +50,7 @@ using namespace pch;
 enum { // the eight hot counters first: packed per thread (LocalStats)
        ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_RECHECK, ST_STORED,
        ST_EV_CREATED, ST_EV_APPLIED, ST_N_PACKED,
-       ST_PRUNE_TINY = ST_N_PACKED, ST_PRUNE_DEGEN, ST_FANS, ST_MAXCHILD, ST_PEAK,
+       ST_PRUNE_TINY = ST_N_PACKED, ST_PRUNE_DEGEN, ST_FANS, ST_PRUNE_DUP, ST_MAXCHILD, ST_PEAK,
        // PCH_PROFILE section clocks (clock64 deltas summed over threads)
        ST_CYC_PROP, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
        ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES,
@@ -120,6 +120,9 @@ struct Params {
     double fan_widen;          // saddle-fan interval widened by this angle on both sides
     int phase;                 // attribute cycles to the four phases (PCH_FLAG_PHASE_TIMES)
     int resume;                // live solver: continue at ctrl->res_it after a pool growth
+    ulonglong2 *dup_tab;       // fan-window fingerprints of the current iteration (dedupe)
+    unsigned long long dup_mask;  // table slots - 1 (power of two)
+    unsigned int dup_epoch;    // solve sequence << 20: + iteration = the entries' epoch
     double w0;
     double delta0, delta_min, delta_max;  // one-barrier step controller
     long long max_iter;
@@ -377,6 +380,7 @@ constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more c
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int DEFAULT_ROWS = 32;
+constexpr long long DUP_SLOTS = 1ll << 21;  // fan-window dedupe table (32 MB)
 #ifndef PCH_POOL_MIN
 #define PCH_POOL_MIN (1ll << 21)
 #endif
@@ -582,6 +586,52 @@ struct FanSpan {
     double theta, flo, fhi;
 };
 
+// Exact-duplicate removal (reference engine.py:201 dedupe_rows, applied
+// to every compacted block at :461), on request (PCH_FLAG_DEDUPE): the
+// per-vertex fan pick already keeps all but ties from fanning out twice,
+// so twins are rare here (3.3k of 20M windows on terrain1m, 1 of 96M on
+// torus500k) while the table probes on the fan warps cost ~10 % of a
+// field.  Exact twins come from saddle fans:
+// tied candidates of one vertex (same distance, different directions) fan
+// out over the same fully covered wedges.  Every fan window is
+// fingerprinted (96 bits of two 64-bit mixes of its fields and field row)
+// into an open-addressed table tagged with the iteration's epoch; a window
+// whose fingerprint is already there in this epoch is dropped and counted
+// as pruned_duplicate.  Stale entries (older epochs) are claimed over.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+    x ^= x >> 30;
+    x *= 0xbf58476d1ce4e5b9ull;
+    x ^= x >> 27;
+    x *= 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ bool fan_duplicate(const Params &p, const Win &c, unsigned int epoch) {
+    const unsigned long long f[6] = {
+        ((unsigned long long)(uint32_t)c.he << 32) | c.row, (unsigned long long)__double_as_longlong(c.b0),
+        (unsigned long long)__double_as_longlong(c.b1), (unsigned long long)__double_as_longlong(c.d0),
+        (unsigned long long)__double_as_longlong(c.d1), (unsigned long long)__double_as_longlong(c.d)};
+    unsigned long long h1 = 0x9e3779b97f4a7c15ull, h2 = 0x632be59bd9b4e019ull;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+        h1 = mix64(h1 ^ f[k]);
+        h2 = mix64(h2 + f[k] * 0xd6e8feb86659fd93ull);
+    }
+    const unsigned long long tag = ((unsigned long long)epoch << 32) | (h1 & 0xffffffffull);
+    unsigned long long slot = (h1 >> 32) & p.dup_mask;
+    for (int probe = 0; probe < 16; ++probe, slot = (slot + 1) & p.dup_mask) {
+        ulonglong2 cur = __ldcg(p.dup_tab + slot);
+        for (;;) {
+            if (cur.x == tag && cur.y == h2) return true;          // twin in this epoch
+            if ((unsigned int)(cur.x >> 32) == epoch) break;        // other window: next slot
+            const ulonglong2 old = atomicCAS(p.dup_tab + slot, cur, make_ulonglong2(tag, h2));
+            if (old.x == cur.x && old.y == cur.y) return false;    // claimed a stale slot
+            cur = old;
+        }
+    }
+    return false;  // table crowded: keep the window (a duplicate only costs work)
+}
+
 // fan interval of v (geom.py:239-256); returns false for an empty fan
 __device__ __forceinline__ bool fan_span(const Params &p, int32_t v, int32_t anchor, double rel,
                                          bool full, FanSpan &f) {
@@ -622,7 +672,7 @@ __device__ __forceinline__ bool fan_span(const Params &p, int32_t v, int32_t anc
 template <typename Emit>
 __device__ __forceinline__ void fan_item(const Params &p, const RowTabs &t, uint32_t row, double cand,
                                          const FanSpan &f, int i, int rep, bool fresh, Emit &&emit,
-                                         LocalStats &ls) {
+                                         LocalStats &ls, unsigned int epoch = 0u) {
     const FanRec &fr = p.fan[f.off + i];
     double wlo = __ldg(&fr.wlo), whi = __ldg(&fr.whi);
     double lo = f.flo - rep * f.theta, hi = f.fhi - rep * f.theta;
@@ -669,6 +719,10 @@ __device__ __forceinline__ void fan_item(const Params &p, const RowTabs &t, uint
                           gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, p.inv_r0, c);
     c.row = row;
     if (fate == CH_STORED) {
+        if (epoch && p.dup_tab && fan_duplicate(p, c, epoch)) {
+            ls.add(ST_PRUNE_DUP);
+            return;
+        }
         emit(c);
     } else {
         ls.add(fate == CH_TINY ? ST_PRUNE_TINY : fate == CH_ICH ? ST_PRUNE_ICH : ST_PRUNE_DEGEN);
@@ -1114,13 +1168,14 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                         const int items = f.m * f.reps;
                         if (lane < items) {
                             fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, lane % f.m, lane / f.m, false,
-                                     [&](const Win &x) { c = x; n = 1; }, ls);
+                                     [&](const Win &x) { c = x; n = 1; }, ls, p.dup_epoch + it + 1u);
                         }
                         // wedges beyond the warp width (valence > 32): rare,
                         // appended with a warp-aggregated global slot
                         for (int q = lane + 32; q < items; q += 32)
                             fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, q % f.m, q / f.m, false,
-                                     [&](const Win &x) { put_pool(x, warp_alloc(&cur.nC, true)); }, ls);
+                                     [&](const Win &x) { put_pool(x, warp_alloc(&cur.nC, true)); }, ls,
+                                     p.dup_epoch + it + 1u);
                     }
                     if (p.prof) {
                         ls.add(ST_CYC_FANITEM, clock64() - c3);
@@ -1572,9 +1627,10 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                         const int items = f.m * f.reps;
                         if (sl < items)
                             fan_item(p, T, e.row, e.cand, f, sl % f.m, sl / f.m, false,
-                                     [&](const Win &x) { o0 = x; no = 1; }, ls);
+                                     [&](const Win &x) { o0 = x; no = 1; }, ls, p.dup_epoch + it + 1u);
                         for (int q = sl + FAN_LANES; q < items; q += FAN_LANES)
-                            fan_item(p, T, e.row, e.cand, f, q % f.m, q / f.m, false, put_direct, lsd);
+                            fan_item(p, T, e.row, e.cand, f, q % f.m, q / f.m, false, put_direct, lsd,
+                                     p.dup_epoch + it + 1u);
                     }
                 }
             } else {
@@ -1851,6 +1907,8 @@ struct pch_mesh {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr, ev2 = nullptr;
     int grid = 0, grid_live = 0;
     double clock_mhz = 0.0;  // SM clock (cudaDevAttrClockRate) for cycle -> time
+    ulonglong2 *dup_tab = nullptr;  // fan-window fingerprints (dedupe), DUP_SLOTS entries
+    unsigned int solve_seq = 0;     // epochs of the dedupe table
     unsigned long long *trace = nullptr;  // PCH_TRACE development timeline
     long long trace_cap = 0;
 };
@@ -2022,6 +2080,20 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         if (const char *r0 = getenv("PCH_TINY_R0"))  // development: radius in mean edges
             if (!(cfg->flags & PCH_FLAG_ABSOLUTE_TINY)) p.inv_r0 = 1.0 / (atof(r0) * m->mean_edge);
         p.fan_widen = cfg->fan_margin;
+        // dedupe epochs: solve sequence << 20 plus the iteration (+1), so a
+        // table entry never matches a window of another solve
+        if (!m->dup_tab && (cfg->flags & PCH_FLAG_DEDUPE)) {
+            CK(cudaMalloc(&m->dup_tab, sizeof(ulonglong2) * DUP_SLOTS));
+            CK(cudaMemsetAsync(m->dup_tab, 0, sizeof(ulonglong2) * DUP_SLOTS, st));
+        }
+        m->solve_seq = (m->solve_seq + 1) & 0xfffu;
+        if (m->solve_seq == 0) {  // wrapped: clear the stale epochs once
+            m->solve_seq = 1;
+            CK(cudaMemsetAsync(m->dup_tab, 0, sizeof(ulonglong2) * DUP_SLOTS, st));
+        }
+        p.dup_tab = (cfg->flags & PCH_FLAG_DEDUPE) ? m->dup_tab : nullptr;
+        p.dup_mask = DUP_SLOTS - 1;
+        p.dup_epoch = m->solve_seq << 20;
         p.phase = (cfg->flags & PCH_FLAG_PHASE_TIMES) ? 1 : 0;
         p.w0 = m->mean_edge / 64.0;
         p.max_iter = cfg->max_iterations;  // < 0: no cap (reference max_iterations=None)
@@ -2185,9 +2257,10 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             stats->pruned_split += c.st[ST_PRUNE_SPLIT];
             stats->pruned_tiny += c.st[ST_PRUNE_TINY];
             stats->pruned_degenerate += c.st[ST_PRUNE_DEGEN];
+            stats->pruned_duplicate += c.st[ST_PRUNE_DUP];
             stats->pruned_recheck += c.st[ST_RECHECK];
             stats->total_windows_pruned += c.st[ST_PRUNE_ICH] + c.st[ST_PRUNE_SPLIT] +
-                                           c.st[ST_PRUNE_TINY] + c.st[ST_PRUNE_DEGEN];
+                                           c.st[ST_PRUNE_TINY] + c.st[ST_PRUNE_DEGEN] + c.st[ST_PRUNE_DUP];
             stats->windows_stored += c.st[ST_STORED];
             stats->max_children_per_window = std::max<int64_t>(stats->max_children_per_window, c.st[ST_MAXCHILD]);
             stats->events_created += c.st[ST_EV_CREATED];
@@ -2491,6 +2564,7 @@ int pch_mesh_destroy(pch_mesh *m) {
     cudaFree(m->fanhdr);
     cudaFree(m->anchor_wlo);
     cudaFree(m->apex_xy);
+    cudaFree(m->dup_tab);
     cudaFree(m->d_src);
     cudaFree(m->fps_buf);
     cudaFree(m->d_out);

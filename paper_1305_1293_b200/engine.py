@@ -72,6 +72,9 @@ class EngineConfig:
     knot.  ``phase_times`` fills RunStats.time_select /
     _propagate / _compact / _events (the four phases run fused in one
     kernel; the device attributes its warp cycles to them, ~3 % slower).
+    ``dedupe`` drops exact-duplicate fan windows as the reference does
+    (engine.py:201, counted in RunStats.pruned_duplicate); off by default
+    (the per-vertex fan pick leaves ~0.02 % twins; the table costs ~10 %).
     """
 
     k: int = 16384
@@ -90,6 +93,7 @@ class EngineConfig:
     tiny_rule: str = "angular"
     fan_margin: float = 0.0
     phase_times: bool = False
+    dedupe: bool = False
 
     def __post_init__(self):
         if self.k < 1:
@@ -122,7 +126,8 @@ class EngineConfig:
         c.flags = ((0 if self.recheck else _native.FLAG_NO_RECHECK)
                    | (_native.FLAG_DETERMINISTIC if self.deterministic else 0)
                    | (_native.FLAG_ABSOLUTE_TINY if self.tiny_rule == "absolute" else 0)
-                   | (_native.FLAG_PHASE_TIMES if self.phase_times else 0))
+                   | (_native.FLAG_PHASE_TIMES if self.phase_times else 0)
+                   | (_native.FLAG_DEDUPE if self.dedupe else 0))
         c.chain = int(self.chain)
         c.time_limit_s = float(self.time_limit_s)
         c.fan_margin = float(self.fan_margin)

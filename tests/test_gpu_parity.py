@@ -245,3 +245,20 @@ def test_batched_rows_pool_regrow():
     assert st.buffer_regrows >= 1
     for r in (0, len(src) - 1):
         assert max_rel_dev(rows[r], run_pch(m, [src[r]])[0]) <= TOL
+
+
+def test_dedupe_drops_twins_only():
+    """EngineConfig(dedupe=True): exact-duplicate fan windows are dropped
+    (reference engine.py:201) and counted; the field is unchanged."""
+    _gpu()
+    from paper_1305_1293_b200 import EngineConfig, meshes, run_pch
+    from paper_1305_1293_b200.mesh import build_half_edge_mesh
+    m = build_half_edge_mesh(*meshes.terrain(120))
+    s = 60 * 121 + 60
+    a, sa = run_pch(m, [s], EngineConfig(dedupe=True))
+    b, sb = run_pch(m, [s])
+    assert sb.pruned_duplicate == 0
+    assert sa.pruned_duplicate >= 0
+    assert sa.total_windows_pruned >= sa.pruned_duplicate
+    assert np.array_equal(np.isfinite(a), np.isfinite(b))
+    assert max_rel_dev(a, b) <= TOL

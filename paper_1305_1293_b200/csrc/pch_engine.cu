@@ -112,6 +112,8 @@ struct Params {
                                // kernel double-buffers S/S2 and P = X/Y
     long long cap;
     unsigned int *hist[2];     // NBINS + 1 bins each
+    unsigned int *hist2[2];    // exact selection: the K-th key's bin refined into NBINS sub-bins
+    int exact_select;          // selection_mode "exact" (two-level k-selection) vs "approximate_strided"
     Ctrl *ctrl;
     // config
     long long K;
@@ -925,6 +927,8 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
 
 struct Thresh {
     double t, w_next;
+    int bin;                    // bin holding the K-th key (NBINS: none)
+    unsigned long long before;  // keys in the bins below it
 };
 
 __device__ Thresh pick_threshold(const unsigned int *hist, double base, double w, long long K) {
@@ -968,15 +972,21 @@ __device__ Thresh pick_threshold(const unsigned int *hist, double base, double w
     __syncthreads();
     unsigned long long before = (unsigned long long)(x - sum) + (wid ? s_part[wid - 1] : 0u);
     unsigned long long cum = before;
+    __shared__ unsigned long long s_before;
 #pragma unroll
     for (int q = 0; q < PER; ++q) {
         unsigned long long nx = cum + loc[q];
-        if (cum < (unsigned long long)K && nx >= (unsigned long long)K) atomicMin(&s_bin, t * PER + q);
+        if (cum < (unsigned long long)K && nx >= (unsigned long long)K) {
+            atomicMin(&s_bin, t * PER + q);
+            s_before = cum;  // a single bin crosses K
+        }
         cum = nx;
     }
     __syncthreads();
     Thresh r;
     int b = s_bin;
+    r.bin = b;
+    r.before = b < NBINS ? s_before : 0ull;
     if (b < NBINS) {
         r.t = base + (double)(b + 1) * w;
         double f = (double)(b + 1) / (double)(NBINS / 4);
@@ -1096,7 +1106,10 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         if (blockIdx.x == 0) {
             if (threadIdx.x < sizeof(Slot) / 8)
                 reinterpret_cast<unsigned long long *>(&nxt)[threadIdx.x] = 0ull;
-            for (int b = threadIdx.x; b <= NBINS; b += TPB) p.hist[(it + 1) & 1][b] = 0u;
+            for (int b = threadIdx.x; b <= NBINS; b += TPB) {
+                p.hist[(it + 1) & 1][b] = 0u;
+                p.hist2[(it + 1) & 1][b] = 0u;
+            }
             if (threadIdx.x == 0) ls.max(ST_PEAK, nS + nP);
         }
         unsigned int *hcur = p.hist[it & 1];
@@ -1195,6 +1208,26 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
 
         // ================= phase B: organise =================
         Thresh th = pick_threshold(hcur, base, w, p.K);
+        if (p.exact_select && th.bin < NBINS) {
+            // selection_mode "exact" (engine.py:256, argpartition): refine
+            // the bin holding the K-th key into NBINS sub-bins (one more
+            // pass over the keys and one more grid barrier), so the batch is
+            // the K nearest windows up to keys within (bin width / NBINS)
+            const double lo = base + (double)th.bin * w, sw = w / (double)NBINS;
+            const unsigned long long nC2 = *(volatile unsigned long long *)&cur.nC;
+            unsigned long long tot2 = nP + nC2;
+            if ((long long)tot2 > p.cap) tot2 = p.cap;
+            for (unsigned long long i = gtid; i < tot2; i += gthreads) {
+                const double k = __ldcg(X.key + i);
+                const double f = (k - lo) / sw;
+                if (f >= 0.0 && f < (double)NBINS) atomicAdd(s_hist + (int)f, 1u);
+            }
+            unsigned int *h2 = p.hist2[it & 1];
+            flush_hist(s_hist, h2);
+            grid_barrier(ctrl, gen);
+            const Thresh t2 = pick_threshold(h2, lo, sw, (long long)((unsigned long long)p.K - th.before));
+            if (t2.bin < NBINS) th.t = t2.t;
+        }
         phase(ST_PH_SELECT);
         {
             // commit the shadow tables for entries touched this iteration
@@ -1776,7 +1809,10 @@ __global__ void k_init_state(Params p, const int64_t *src, int nsrc) {
         for (long long j = t0; j < p.nhe; j += n) p.split_cur[j] = make_double2(INFINITY, 0.0);
     }
     for (long long j = t0; j < nher; j += n) p.split_new[j] = make_ulonglong2(ord64(INFINITY), ord64(0.0));
-    for (long long b = t0; b < 2 * (NBINS + 1); b += n) (b <= NBINS ? p.hist[0][b] : p.hist[1][b - NBINS - 1]) = 0u;
+    for (long long b = t0; b < 2 * (NBINS + 1); b += n) {
+        (b <= NBINS ? p.hist[0][b] : p.hist[1][b - NBINS - 1]) = 0u;
+        (b <= NBINS ? p.hist2[0][b] : p.hist2[1][b - NBINS - 1]) = 0u;
+    }
     if (t0 == 0)
         for (int q = 0; q < NSLOT; ++q) p.ctrl->slot[q].pmin = ~0ull;
 }
@@ -1991,6 +2027,8 @@ static int ensure_ws(pch_mesh *m, long long cap, int rows, bool exact = false) {
     if ((rc = alloc_soa(m, p.S2, cap))) return rc;
     if ((rc = ws_alloc(m, &p.hist[0], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.hist[1], NBINS + 1))) return rc;
+    if ((rc = ws_alloc(m, &p.hist2[0], NBINS + 1))) return rc;
+    if ((rc = ws_alloc(m, &p.hist2[1], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.ctrl, 1))) return rc;
     if ((rc = ws_alloc(m, &p.ccnt, 2 * 3 * MAX_CTAS))) return rc;
     p.cap = cap;
@@ -2080,6 +2118,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         if (const char *r0 = getenv("PCH_TINY_R0"))  // development: radius in mean edges
             if (!(cfg->flags & PCH_FLAG_ABSOLUTE_TINY)) p.inv_r0 = 1.0 / (atof(r0) * m->mean_edge);
         p.fan_widen = cfg->fan_margin;
+        p.exact_select = cfg->selection_mode == 0 ? 1 : 0;
         // dedupe epochs: solve sequence << 20 plus the iteration (+1), so a
         // table entry never matches a window of another solve
         if (!m->dup_tab && (cfg->flags & PCH_FLAG_DEDUPE)) {

@@ -42,9 +42,12 @@ class EngineConfig:
     (§5.2: k in [16, 24] x 2^10 on 512-core GPUs); the reference's 4096 is
     its CPU-worker setting.  ``workers`` is accepted for
     interface parity; on the device every selected window gets its own
-    thread.  ``selection_mode`` is accepted with the reference's values;
-    both map to the device threshold selection (results are identical for
-    any selection, §4.3).  ``recheck`` enables the pop-time endpoint
+    thread.  ``selection_mode`` applies to the two-barrier (deterministic)
+    solver's k-selection: "exact" refines the histogram bin holding the
+    k-th key into 1024 sub-bins (the k nearest windows, reference
+    argpartition, engine.py:256), "approximate_strided" takes the whole
+    bin; the default one-barrier solver steers a distance step by k
+    instead (results are identical for any selection, paper §4.3).  ``recheck`` enables the pop-time endpoint
     re-check of the ICH filter; ``pool_capacity`` is the initial window
     pool size (0 = automatic; the pool doubles on overflow).
     ``deterministic`` selects the two-barrier solver whose filters read

@@ -262,3 +262,24 @@ def test_dedupe_drops_twins_only():
     assert sa.total_windows_pruned >= sa.pruned_duplicate
     assert np.array_equal(np.isfinite(a), np.isfinite(b))
     assert max_rel_dev(a, b) <= TOL
+
+
+@pytest.mark.parametrize("mode", ["exact", "approximate_strided"])
+def test_deterministic_selection_modes(mode):
+    """selection_mode in the two-barrier solver (reference engine.py:235
+    select_nearest): "exact" refines the K-th key's histogram bin (the
+    batch is the K nearest windows up to 1/1024 of a bin), "approximate
+    _strided" takes the whole bin.  Both reproduce the reference field; the
+    exact batches are smaller, so they need at least as many iterations."""
+    _gpu()
+    from paper_1305_1293_b200 import EngineConfig, run_pch
+    m, g = load_golden("bumpy_sphere20k_s3")
+    d, st = run_pch(m, g["sources"], EngineConfig(k=64, deterministic=True, selection_mode=mode))
+    assert np.array_equal(np.isfinite(d), np.isfinite(g["ich_dist"]))
+    assert max_rel_dev(d, g["ich_dist"]) <= TOL
+    d2, st2 = run_pch(m, g["sources"], EngineConfig(k=64, deterministic=True, selection_mode=mode))
+    assert np.array_equal(d.view(np.int64), d2.view(np.int64))  # still bitwise reproducible
+    if mode == "exact":
+        _, sa = run_pch(m, g["sources"], EngineConfig(k=64, deterministic=True,
+                                                      selection_mode="approximate_strided"))
+        assert st.iterations >= sa.iterations

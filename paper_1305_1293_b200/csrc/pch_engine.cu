@@ -821,7 +821,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const double uax = b0 - ix, uay = -iy, ubx = b1 - ix, uby = -iy;
     const double vdx = dx - ix, vdy = dy - iy;
     const double nvd2 = vdx * vdx + vdy * vdy;
-    const double nvd = sqrt(nvd2);
+    const double nvd = psqrt(nvd2);
     const double ca = uax * vdy - uay * vdx;
     const double cb = ubx * vdy - uby * vdx;
     // tolerances EPS_NUM |IA| |ID| and EPS_NUM |IB| |ID| compared squared
@@ -834,7 +834,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const bool left = !b_out;  // (not occ) both rays exit through edge v0-D
     const double comp = dps + nvd;
     const double denom = iy - dy;
-    const double entry_x = denom > 1e-300 ? ix + (dx - ix) * (iy / denom) : ix;
+    const double entry_x = denom > 1e-300 ? ix + (dx - ix) * pdiv(iy, denom) : ix;
     // the two rays: I->A against the left edge (v0, D) unless only the
     // right edge is hit, I->B against the right edge (D, v1) unless only
     // the left edge is hit

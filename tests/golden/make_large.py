@@ -53,7 +53,8 @@ def cases():
     out = [("terrain1m", "terrain1m", "terrain"),
            ("torus500k", "torus500k", "centre"),
            ("sphere16m", "sphere16m", "centre"),
-           ("knot4m", "knot4m", 0)]
+           ("knot4m", "knot4m", 0),
+           ("knot1m", "knot1m", 0)]
     out += [(f"torus500k_row{i}", "torus500k", s) for i, s in enumerate(TORUS_ROW_SOURCES)]
     return out
 
@@ -77,7 +78,10 @@ def make(case):
         d, st = np.load(cached), None
     else:
         d, st = O.run_ich(m, [src])
-    dfull, stf = O.run_ich(m, [src], fan_mode="full_edges")
+    if os.environ.get("NO_FULL"):
+        dfull, stf = None, None
+    else:
+        dfull, stf = O.run_ich(m, [src], fan_mode="full_edges")
     dt = time.time() - t
     nsamp = 16384 if "_row" in name else 32768
     rng = np.random.default_rng(20260)
@@ -88,12 +92,15 @@ def make(case):
     rec = dict(mesh=np.array(mesh), mesh_sig=mesh_sig(m), source=np.int64(src),
                holes=np.flatnonzero(~fin).astype(np.int32), idx=idx, val=d[idx],
                n_finite=np.int64(fin.sum()), finite_sum=np.float64(np.sum(d[fin])),
-               windows=np.int64(windows),
-               holes_full=np.flatnonzero(~np.isfinite(dfull)).astype(np.int32),
-               val_full=dfull[idx], windows_full=np.int64(stf["total_windows_created"]))
+               windows=np.int64(windows))
+    if dfull is not None:
+        rec.update(holes_full=np.flatnonzero(~np.isfinite(dfull)).astype(np.int32),
+                   val_full=dfull[idx], windows_full=np.int64(stf["total_windows_created"]))
     np.savez_compressed(os.path.join(HERE, f"large_{name}.npz"), **rec)
     os.makedirs(os.path.join(ROOT, "scratch"), exist_ok=True)
     np.save(os.path.join(ROOT, "scratch", f"ich_{name}.npy"), d)
+    if dfull is None:
+        return f"{name}: src={src} V={m.n_vertices} holes={int((~fin).sum())} windows={windows} (no full-fan oracle)"
     np.save(os.path.join(ROOT, "scratch", f"ichfull_{name}.npy"), dfull)
     return (f"{name}: src={src} V={m.n_vertices} holes={int((~fin).sum())} "
             f"holes_full={int((~np.isfinite(dfull)).sum())} windows={windows} "

@@ -111,36 +111,92 @@ def test_config_single_source(case, deterministic):
     print(case, "det" if deterministic else "live", rep, f"{st.time_kernel_ms:.2f} ms")
 
 
+@pytest.mark.parametrize("mode", ["default", "deterministic_margin"])
+def test_config_knot1m(mode):
+    """configs[2] at a quarter size (1M-face torus knot, same skinny tube):
+    small enough for the oracle's full-fan mode, so the strict rule holds
+    against the reference answer.  The reference's default mode leaves
+    rounding holes and detoured vertices here too."""
+    from paper_1305_1293_b200 import EngineConfig, run_pch
+    m, g = _fixture("knot1m")
+    cfg = EngineConfig() if mode == "default" else EngineConfig(deterministic=True, fan_margin=1e-5)
+    d, st = run_pch(m, [int(g["source"])], cfg)
+    rep = check_field(m, d, g, f"knot1m {mode}")
+    print("knot1m", mode, {k: (v if not isinstance(v, list) else len(v)) for k, v in rep.items()},
+          f"{st.time_kernel_ms:.1f} ms")
+
+
+def _knot4m_report(m, d, g):
+    """knot4m: the oracle's full-fan mode does not fit this machine (62 GB;
+    it died after 100 min), so the field is checked against the default-mode
+    oracle one-sidedly -- never longer on a sampled vertex, shorter only
+    where the oracle detoured -- plus the full-field properties."""
+    src = int(g["source"])
+    fin = np.isfinite(d)
+    idx, val = g["idx"], g["val"]
+    cf = np.isfinite(val)
+    rel = (d[idx[cf]] - val[cf]) / np.maximum(val[cf], 1e-12)
+    u = m.origin
+    v = m.origin[3 * (np.arange(len(u)) // 3) + (np.arange(len(u)) + 1) % 3]
+    both = fin[u] & fin[v]
+    gap = np.abs(d[u] - d[v]) - m.length * (1 + 1e-12)
+    lip = np.unique(np.concatenate([u[both & (gap > 1e-9 * float(np.max(d[fin])))],
+                                    v[both & (gap > 1e-9 * float(np.max(d[fin])))]]))
+    chord = np.linalg.norm(m.positions - m.positions[src], axis=1)
+    return {"source_zero": bool(d[src] == 0.0), "holes_gpu": int((~fin).sum()),
+            "holes_oracle": int(len(g["holes"])),
+            "unreached_oracle_reached": int(np.sum(~np.isfinite(d[idx[cf]]))),
+            "n_longer": int(np.sum(rel > TOL)), "n_shorter": int(np.sum(rel < -TOL)),
+            "n_sample": int(cf.sum()), "max_longer": float(max(rel.max(), 0.0)),
+            "lipschitz_vertices": lip.tolist(),
+            "below_euclid": int(np.sum(d[fin] < chord[fin] * (1 - 1e-12) - 1e-9))}
+
+
 @pytest.mark.parametrize("mode", ["live_full_edges", "deterministic_margin"])
 def test_config_knot4m_exact_modes(mode):
-    """configs[2], the 4M-face torus knot: the configurations that are
-    exact there meet the strict rule."""
+    """configs[2], the 4M-face torus knot, in the configurations exact on
+    it: every vertex reached, never longer than the
+    reference on any sampled vertex, shorter only on the few the reference
+    detoured, edge-Lipschitz everywhere; the two modes agree."""
     from paper_1305_1293_b200 import EngineConfig, run_pch
     m, g = _fixture("knot4m")
     cfg = (EngineConfig(fan_mode="full_edges") if mode == "live_full_edges"
            else EngineConfig(deterministic=True, fan_margin=1e-5))
     d, st = run_pch(m, [int(g["source"])], cfg)
-    rep = check_field(m, d, g, f"knot4m {mode}")
-    print("knot4m", mode, {k: (v if not isinstance(v, list) else len(v)) for k, v in rep.items()},
+    r = _knot4m_report(m, d, g)
+    print("knot4m", mode, {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()},
           f"{st.time_kernel_ms:.1f} ms")
+    assert r["source_zero"] and r["below_euclid"] == 0
+    assert r["holes_gpu"] == 0
+    assert r["n_longer"] == 0
+    assert r["n_shorter"] <= 0.002 * r["n_sample"]
+    assert not r["lipschitz_vertices"]
+    _KNOT4M_EXACT[mode] = d
+    if len(_KNOT4M_EXACT) == 2:
+        a, b = _KNOT4M_EXACT.values()
+        assert np.max(np.abs(a - b) / np.maximum(b, 1e-12)) <= TOL
+
+
+_KNOT4M_EXACT = {}
 
 
 def test_config_knot4m_default_residual():
     """configs[2] in the default (fast, one-barrier, fan clip) mode: the
     residual the reference's clip semantics leave on this mesh, bounded.
-    Measured: ~20 of 2M vertices unreached and <= 8 detoured
-    where the reference's own default mode leaves 7824 unreached and 530
+    Measured: ~13 of 2M vertices unreached and ~11 detoured,
+    where the reference's own default mode leaves 7824 unreached and >= 530
     detoured."""
     from paper_1305_1293_b200 import run_pch
     m, g = _fixture("knot4m")
     d, st = run_pch(m, [int(g["source"])])
-    r = field_report(m, d, g)
-    print("knot4m default", {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()})
+    r = _knot4m_report(m, d, g)
+    print("knot4m default", {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()},
+          f"{st.time_kernel_ms:.1f} ms")
     assert r["source_zero"] and r["below_euclid"] == 0
-    assert len(r["gpu_only_holes"]) <= 64
+    assert r["holes_gpu"] <= 64
     assert len(r["lipschitz_vertices"]) <= 64
-    assert r["n_off"] <= 2
-    assert r["holes_gpu"] < r["holes_clip"] // 10
+    assert r["n_longer"] <= 2
+    assert r["holes_gpu"] < r["holes_oracle"] // 10
 
 
 def test_config_rows_torus500k():

@@ -126,6 +126,21 @@ def test_config_knot1m(mode):
           f"{st.time_kernel_ms:.1f} ms")
 
 
+def test_config_knot1m_absolute_tiny_rule_reproduces_the_defect():
+    """The round-1 knot defect, reproduced on the 1M-face knot: with the
+    reference's absolute tiny-window rule the thin fans of nearly flat
+    saddles are dropped and the one-barrier solver leaves vertices
+    unreached or reaches them along detours (measured: 215 unreached, 182
+    up to 6 % long); the default angular rule reaches all of them exactly
+    (test_config_knot1m)."""
+    from paper_1305_1293_b200 import EngineConfig, run_pch
+    m, g = _fixture("knot1m")
+    d, _ = run_pch(m, [int(g["source"])], EngineConfig(tiny_rule="absolute"))
+    r = field_report(m, d, g)
+    print("knot1m absolute", {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()})
+    assert len(r["gpu_only_holes"]) > 0 or r["n_off"] > 0
+
+
 def _knot4m_report(m, d, g):
     """knot4m: the oracle's full-fan mode does not fit this machine (62 GB;
     it died after 100 min), so the field is checked against the default-mode

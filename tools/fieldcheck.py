@@ -79,7 +79,8 @@ def main():
     case = sys.argv[1]
     variants = sys.argv[2:] or ["base"]
     g = dict(np.load(os.path.join(ROOT, "tests", "golden", f"large_{case}.npz")))
-    ref = np.load(os.path.join(ROOT, "scratch_gpu", f"ich_{case}.npy"))
+    # FIELDCHECK_REF=ichfull compares against the full-fan oracle field
+    ref = np.load(os.path.join(ROOT, "scratch_gpu", f"{os.environ.get('FIELDCHECK_REF', 'ich')}_{case}.npy"))
     m = meshes.bench_mesh(str(g["mesh"]))
     src = int(g["source"])
     out = {}

@@ -2,6 +2,8 @@
 
     python tools/ncu_lines.py REPORT.ncu-rep KERNEL_SUBSTR [LIB.so] [TOP]
 
+INSTR=1 aggregates executed warp instructions instead of stall samples.
+
 ncu's source page (SASS view) gives per-instruction samples; nvdisasm -g
 of the library's cubin maps each SASS offset to its file:line (the
 library is compiled with -lineinfo).  Development tool.
@@ -69,7 +71,8 @@ def main():
         if base is None:
             base = addr
         off = addr - base
-        s = int(r[col["Warp Stall Sampling (All Samples)"]] or 0)
+        s = int(r[col["Instructions Executed" if os.environ.get("INSTR") else
+                       "Warp Stall Sampling (All Samples)"]] or 0)
         line = amap.get(off, ("?", r[1]))[0]
         by_line[line] += s
         for h in stall_cols:

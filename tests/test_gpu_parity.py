@@ -51,12 +51,18 @@ def test_golden_parity(name, k):
         assert max_rel_dev(d, ref) <= TOL, name
     else:
         # shadowed boundary (reflex boundary vertices the reference never
-        # bends around): the reference's own two engines disagree there
-        # (schedule-dependent pruning, tests/test_oracle_golden.py), so the
-        # field is only checked to reach every vertex both reach, with
-        # distances of the same shape
+        # bends around): the reference's own two engines disagree on which
+        # vertices they reach and, at a few, on the route around the shadow
+        # (schedule-dependent pruning, tests/test_oracle_golden.py).  Every
+        # vertex both reach, the GPU reaches; where they agree the GPU is
+        # within 1e-9 of them; where they disagree it lies between them
+        pch = g["pch_dist"]
         assert np.all(np.isfinite(d[mask])), name
-        assert max_rel_dev(d[mask], g["pch_dist"][mask]) < 1e-2
+        agree = mask & (np.abs(ref - pch) <= TOL * np.maximum(np.abs(ref), 1e-12))
+        assert max_rel_dev(d[agree], ref[agree]) <= TOL, name
+        lo, hi = np.minimum(ref, pch), np.maximum(ref, pch)
+        split = mask & ~agree
+        assert np.all(d[split] >= lo[split] * (1 - TOL)) and np.all(d[split] <= hi[split] * (1 + TOL)), name
     src = np.asarray(g["sources"])
     assert np.all(d[src] == 0.0)
     assert st.iterations >= 1 and st.windows_propagated >= 1
@@ -283,3 +289,54 @@ def test_deterministic_selection_modes(mode):
         _, sa = run_pch(m, g["sources"], EngineConfig(k=64, deterministic=True,
                                                       selection_mode="approximate_strided"))
         assert st.iterations >= sa.iterations
+
+
+def test_device_sources_validated():
+    """an out-of-range index in a device-resident source list
+    fails the solve with PCH_ERR_SOURCE (ValueError) instead of writing out
+    of bounds; the mesh stays usable."""
+    _gpu()
+    import torch
+    from paper_1305_1293_b200 import run_pch, run_pch_device, run_pch_rows_device
+    m, g = load_golden("icosphere1280_s85")
+    out = torch.empty(m.n_vertices, dtype=torch.float64, device="cuda:0")
+    for bad in (-1, m.n_vertices, 1 << 40):
+        src = torch.tensor([0, bad], dtype=torch.int64, device="cuda:0")
+        with pytest.raises(ValueError):
+            run_pch_device(m, src.data_ptr(), 2, out.data_ptr())
+        rows = torch.empty((2, m.n_vertices), dtype=torch.float64, device="cuda:0")
+        with pytest.raises(ValueError):
+            run_pch_rows_device(m, src.data_ptr(), 2, rows.data_ptr())
+    d, _ = run_pch(m, g["sources"])
+    assert max_rel_dev(d, g["ich_dist"]) <= TOL
+
+
+def test_max_iterations_reference_semantics():
+    """ADVICE r1 / reference engine.py:475: None = no cap, 0 = a real cap
+    (the guard trips after the first iteration); the optional wall-time
+    guard is off by default."""
+    _gpu()
+    from paper_1305_1293_b200 import EngineConfig, EngineGuard, run_pch
+    m, g = load_golden("icosphere1280_s85")
+    with pytest.raises(EngineGuard):
+        run_pch(m, g["sources"], EngineConfig(max_iterations=0))
+    d, st = run_pch(m, g["sources"], EngineConfig(max_iterations=None))
+    assert max_rel_dev(d, g["ich_dist"]) <= TOL
+    d, _ = run_pch(m, g["sources"], EngineConfig(max_iterations=st.iterations))
+    assert max_rel_dev(d, g["ich_dist"]) <= TOL
+
+
+def test_phase_times_reported():
+    """RunStats.time_select / _propagate / _compact / _events (reference
+    engine.py:470-473) with phase_times=True: positive, summing to the
+    kernel time; zero (not measured) by default."""
+    _gpu()
+    from paper_1305_1293_b200 import EngineConfig, run_pch
+    m, g = load_golden("icosphere20480_s1370")
+    _, st = run_pch(m, g["sources"], EngineConfig(phase_times=True))
+    parts = [st.time_select, st.time_propagate, st.time_compact, st.time_events]
+    assert all(x >= 0.0 for x in parts) and st.time_propagate > 0.0
+    assert abs(sum(parts) * 1e3 - st.time_kernel_ms) <= 1e-6 * max(st.time_kernel_ms, 1.0) + 1e-9
+    assert st.prop_item_us > 0.0
+    _, st0 = run_pch(m, g["sources"])
+    assert st0.time_propagate == 0.0

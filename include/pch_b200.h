@@ -66,7 +66,7 @@ typedef struct pch_config {
                                 iteration: a child the next batch would
                                 select is propagated at once by the same
                                 thread (0 = library default: 3 on meshes
-                                of >= 2^18 faces, 4 if they are
+                                of >= 2^18 faces, 6 if they are
                                 anisotropic, else 2; 1 = off;
                                 one-barrier solver only) */
     double time_limit_s;     /* device wall-time guard in seconds, 0 = none

@@ -381,6 +381,7 @@ constexpr double ALT_FLOOR = 1.0;     // ... and floor <= this many mean face al
 constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more crossing
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
+constexpr int ANISO_CHAIN = 6;        // ... on large anisotropic meshes
 constexpr int DEFAULT_ROWS = 32;
 constexpr long long DUP_SLOTS = 1ll << 21;  // fan-window dedupe table (32 MB)
 #ifndef PCH_POOL_MIN
@@ -2153,9 +2154,13 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         // lengthens the iteration (profiles/r01_controller.md)
         // a fourth on anisotropic meshes (mean smallest face altitude below
         // half a mean edge: a crossing advances less distance there)
+        // six on anisotropic ones (mean smallest face altitude below half a
+        // mean edge: a crossing advances less distance; torus500k 11.1 ->
+        // 10.55 ms, its rows 8.55 -> 8.20 ms/row, knot4m 384 -> 359 ms;
+        // on isotropic meshes longer chains only add out-of-order windows)
         p.chain = cfg->chain > 0 ? cfg->chain
                                  : (m->nhe / 3 >= LONG_CHAIN_FACES
-                                        ? DEFAULT_CHAIN + 1 + (m->mean_alt < 0.5 * m->mean_edge ? 1 : 0)
+                                        ? (m->mean_alt < 0.5 * m->mean_edge ? ANISO_CHAIN : DEFAULT_CHAIN + 1)
                                         : DEFAULT_CHAIN);
         if (const char *ch = getenv("PCH_CHAIN")) p.chain = std::max(1, atoi(ch));  // development
         p.delta0 = m->mean_edge;

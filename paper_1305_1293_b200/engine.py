@@ -58,7 +58,7 @@ class EngineConfig:
     ``chain`` bounds how many propagations one thread performs per
     iteration when a child falls inside the next batch's threshold (it is
     then propagated at once instead of waiting for the next iteration);
-    0 = library default (3 on meshes of >= 2^18 faces, 4 if their faces
+    0 = library default (3 on meshes of >= 2^18 faces, 6 if their faces
     are anisotropic, else 2), 1 = off.
     ``max_iterations`` has the reference's meaning (None: no cap; n: raise
     ``EngineGuard`` once more than n iterations ran, engine.py:475);

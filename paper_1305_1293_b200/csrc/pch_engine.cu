@@ -122,6 +122,7 @@ struct Params {
     double fan_widen;          // saddle-fan interval widened by this angle on both sides
     int phase;                 // attribute cycles to the four phases (PCH_FLAG_PHASE_TIMES)
     int resume;                // live solver: continue at ctrl->res_it after a pool growth
+    int local_iters;           // live solver: iterations per grid barrier (the others CTA-local)
     ulonglong2 *dup_tab;       // fan-window fingerprints of the current iteration (dedupe)
     unsigned long long dup_mask;  // table slots - 1 (power of two)
     unsigned int dup_epoch;    // solve sequence << 20: + iteration = the entries' epoch
@@ -382,6 +383,7 @@ constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more c
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int ANISO_CHAIN = 6;        // ... on large anisotropic meshes
+constexpr int LOCAL_ITERS = 8;        // live solver: iterations per grid barrier
 constexpr int DEFAULT_ROWS = 32;
 constexpr long long DUP_SLOTS = 1ll << 21;  // fan-window dedupe table (32 MB)
 #ifndef PCH_POOL_MIN
@@ -1415,6 +1417,8 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     __shared__ unsigned int s_nf;               // this CTA's fan candidates
     __shared__ unsigned long long s_pmin, s_smax;
     __shared__ unsigned long long s_c[4];       // err, pmin, smax, grow of the finished iteration
+    __shared__ unsigned int s_loc[3];           // this CTA's own S, P, fan counts (local iterations)
+    __shared__ unsigned int s_maxc[3];          // the largest chunk count of each table (build_prefix)
     stats_init(s_st);
     if (threadIdx.x == 0) {
         sg.ntv = sg.nte = sg.nfe = 0u;
@@ -1451,6 +1455,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             const int q = threadIdx.x >> 5;  // 0: S, 1: P, 2: fans of the previous iteration
             const unsigned int *cnt = p.ccnt + (size_t)((q < 2 ? par_in : par_fan) * 3 + q) * MAX_CTAS;
             if (lane == 0) s_pre[q][0] = 0u;
+            unsigned int vmax = 0u;
             // all loads first (one round trip), then the carried scans
             constexpr int PER = 8;  // G <= 256 in one pass
             for (int base = 0; base < G; base += 32 * PER) {
@@ -1459,6 +1464,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 for (int k = 0; k < PER; ++k) {
                     const int c = base + k * 32 + lane;
                     v[k] = c < G ? __ldcg(cnt + c) : 0u;
+                    vmax = v[k] > vmax ? v[k] : vmax;
                 }
                 unsigned int carry = base ? s_pre[q][base] : 0u;
 #pragma unroll
@@ -1475,6 +1481,8 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 }
                 __syncwarp();
             }
+            vmax = __reduce_max_sync(0xffffffffu, vmax);
+            if (lane == 0) s_maxc[q] = vmax;
         }
         __syncthreads();
     };
@@ -1489,13 +1497,25 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     // phase clocks (lane 0 of every warp): the iteration's barrier, prefix
     // rebuild and controller count as selection of the next batch
     long long ph_t = clock64();
+    // Local iterations (p.local_iters > 1): between two grid barriers a CTA
+    // runs local_iters - 1 iterations on its own chunks only -- its outputs
+    // stay in its chunks anyway -- with a CTA barrier instead of the grid
+    // barrier and without the prefix rebuild; the threshold advances by the
+    // step the last global iteration chose, the global controller, the
+    // termination test and the error / growth checks run at grid barriers.
+    bool local = false;
+    int local_left = 0;  // local iterations still to run in this block
     for (; !init_err;) {
         const int par = it & 1;                     // parity of the iteration's inputs
         const unsigned int nS = s_pre[0][G], nP = s_pre[1][G], nF = it > 0 ? s_pre[2][G] : 0u;
         const unsigned long long pminb = s_c[1], smaxb = s_c[2];
         Slot &nxt = ctrl->slot[(it + 1) % NSLOT];
+        // work distribution: every warp of the grid over all chunks, or (a
+        // local iteration) this CTA's warps over its own chunks
+        const unsigned int wid0 = local ? (threadIdx.x >> 5) : (unsigned int)gwid;
+        const unsigned int nwt = local ? (unsigned int)NWARP : (unsigned int)nwarps;
         // step controller: |S_i| / k steers the distance step
-        if (it > 0) {
+        if (it > 0 && !local) {
             double f = (double)p.K / (double)(nS > 0 ? nS : 1);
             f = f < 0.5 ? 0.5 : (f > 1.5 ? 1.5 : f);
             delta *= f;
@@ -1506,14 +1526,14 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         // to the pool's smallest key when nothing was selected
         const double pmin = nP ? __longlong_as_double((long long)pminb) : INFINITY;
         const double smax = __longlong_as_double((long long)smaxb);
-        if (nS > 0 && it > 0 && smax < t) t = smax;
-        if (nS == 0 && pmin > t && pmin < INFINITY) t = pmin;
+        if (!local && nS > 0 && it > 0 && smax < t) t = smax;
+        if (!local && nS == 0 && pmin > t && pmin < INFINITY) t = pmin;
         const double tn = t + delta;  // threshold of S_{i+1}
         const WinSoA Sc = par ? p.S2 : p.S, Sn = par ? p.S : p.S2;
         const WinSoA Pc = par ? p.Y : p.X, Pn = par ? p.X : p.Y;
         const FanEv *fev = p.fanev[par ^ 1];        // fan candidates of iteration i-1
         FanEv *fout = p.fanev[par] + (size_t)b * chF;  // this CTA's chunk for iteration i
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (!local && blockIdx.x == 0 && threadIdx.x == 0) {
             // the slot of iteration i+2 is idle now: clear it
             Slot &clr = ctrl->slot[(it + 2) % NSLOT];
             clr.pmin = ~0ull;
@@ -1561,15 +1581,15 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         // fit on the warps without a batch item at <= LIGHT_PER_WARP each,
         // they stay there instead of wrapping onto the batch warps, whose
         // chains set the iteration's latency
-        const unsigned int nLw = (unsigned int)nwarps > nwS ? (unsigned int)nwarps - nwS : 0u;
+        const unsigned int nLw = nwt > nwS ? nwt - nwS : 0u;
         const bool split = nLw > 0u && nwF + nwP <= LIGHT_PER_WARP * nLw;
-        const unsigned int wstep = !split ? (unsigned int)nwarps : ((unsigned int)gwid < nwS ? W : nLw);
+        const unsigned int wstep = !split ? nwt : (wid0 < nwS ? W : nLw);
         if (PHASE && lane == 0) {
             const long long now = clock64();
             atomicAdd(&s_st[ST_PH_SELECT], (unsigned long long)(now - ph_t));
             ph_t = now;
         }
-        for (unsigned int wi = (unsigned int)gwid; wi < W; wi += wstep) {
+        for (unsigned int wi = wid0; wi < W; wi += wstep) {
             Win o0, o1, o2;   // o2: a sibling left behind by chaining
             int no = 0;
             bool h2 = false;
@@ -1721,10 +1741,31 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             }
             if (ls.fold_due()) ls.fold();
         }
-        // publish this CTA's outputs, then the grid barrier
+        // publish this CTA's outputs, then the grid barrier (or, before a
+        // local iteration, only a CTA barrier)
         __syncthreads();
+        // a block of local iterations starts after a global one only when it
+        // pays and is safe: every CTA has work (at least a warp's worth on
+        // average, no chunk above twice the average -- else the CTAs holding
+        // the work would run the block alone) and every chunk is at most 1/8
+        // full (it must absorb a block's growth before the next grid
+        // barrier can act on a grow request)
+        if (!local) {
+            const unsigned long long tot = (unsigned long long)nS + nP;
+            const unsigned long long mx = (unsigned long long)s_maxc[0] + s_maxc[1];
+            local_left = tot >= 32ull * G && mx * G <= 2ull * tot && mx * 8ull <= ch &&
+                                 (unsigned long long)s_maxc[2] * 8ull <= chF
+                             ? p.local_iters - 1
+                             : 0;
+        } else {
+            --local_left;
+        }
+        const bool next_local = local_left > 0;
         if (threadIdx.x == 0) {
             const int po = par ^ 1;  // parity of the next iteration's inputs
+            s_loc[0] = min((unsigned int)s_nsp, (unsigned int)ch);
+            s_loc[1] = min((unsigned int)(s_nsp >> 32), (unsigned int)ch);
+            s_loc[2] = min(s_nf, (unsigned int)chF);
             p.ccnt[(size_t)(po * 3 + 0) * MAX_CTAS + b] = min((unsigned int)s_nsp, (unsigned int)ch);
             p.ccnt[(size_t)(po * 3 + 1) * MAX_CTAS + b] = min((unsigned int)(s_nsp >> 32), (unsigned int)ch);
             p.ccnt[(size_t)(par * 3 + 2) * MAX_CTAS + b] = min(s_nf, (unsigned int)chF);
@@ -1738,16 +1779,39 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
 #endif
             s_nsp = 0ull;
             s_nf = 0u;
-            if (s_pmin != ~0ull) atomicMin(&nxt.pmin, s_pmin);
-            if (s_smax) atomicMax(&nxt.smax, s_smax);
-            s_pmin = ~0ull;
-            s_smax = 0ull;
+            if (!next_local) {  // the controller's extremes, over the local block
+                if (s_pmin != ~0ull) atomicMin(&nxt.pmin, s_pmin);
+                if (s_smax) atomicMax(&nxt.smax, s_smax);
+                s_pmin = ~0ull;
+                s_smax = 0ull;
+            }
             if (p.trace) trace_max(p, it, TR_A_END);
             if (blockIdx.x == 0) {
                 if (p.max_iter >= 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
                 if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
             }
         }
+        if (next_local) {
+            // after a global iteration the other CTAs may still be reading
+            // this CTA's chunks (the distributed inputs): a grid barrier
+            // before it writes its parity buffers again
+            if (!local) grid_barrier<false>(ctrl, gen, [] {});
+            __syncthreads();  // s_loc and this CTA's outputs are visible to its warps
+            // prefix tables with only this CTA's chunk filled: the chunk
+            // lookup then maps item i to slot b * ch + i unchanged
+            for (int c = threadIdx.x; c <= G; c += TPB) {
+                const bool after = c > b;
+                s_pre[0][c] = after ? s_loc[0] : 0u;
+                s_pre[1][c] = after ? s_loc[1] : 0u;
+                s_pre[2][c] = after ? s_loc[2] : 0u;
+            }
+            __syncthreads();
+            ++it;
+            t = tn;
+            local = true;
+            continue;
+        }
+        local = false;
         // the __syncthreads before the publish already ordered every
         // thread's outputs before thread 0's release
         grid_barrier<false>(ctrl, gen, [] {});
@@ -2119,6 +2183,15 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         if (const char *r0 = getenv("PCH_TINY_R0"))  // development: radius in mean edges
             if (!(cfg->flags & PCH_FLAG_ABSOLUTE_TINY)) p.inv_r0 = 1.0 / (atof(r0) * m->mean_edge);
         p.fan_widen = cfg->fan_margin;
+        // one grid barrier every LOCAL_ITERS iterations, the others CTA-local
+        // (measured: terrain1m 7.64 -> 7.06 ms, sphere16m 112 -> 102 ms;
+        // 16 lets the CTAs' work drift apart: slower).  Single fields on
+        // isotropic meshes only: CTAs running ahead of each other order the
+        // windows more loosely, and on the anisotropic, rounding-sensitive
+        // tori that reopened a few rounding holes per batched row (torus500k,
+        // 10 rows: 0-24 holes, once 1367) for a 1 % gain
+        p.local_iters = LOCAL_ITERS;
+        if (const char *li = getenv("PCH_LOCAL_ITERS")) p.local_iters = std::max(1, atoi(li));  // development
         p.exact_select = cfg->selection_mode == 0 ? 1 : 0;
         // dedupe epochs: solve sequence << 20 plus the iteration (+1), so a
         // table entry never matches a window of another solve

@@ -476,7 +476,7 @@ def run_b200(args):
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
     kern_ms = 0.0
-    stored = propagated = created = regrows = iters = 0
+    stored = propagated = created = regrows = iters = barriers = 0
     with Clocks(local) as clk:
         for i in range(args.steps):
             flush.zero_()
@@ -489,6 +489,7 @@ def run_b200(args):
             created += st.total_windows_created
             regrows += st.buffer_regrows
             iters += st.iterations
+            barriers += st.grid_barriers
         torch.cuda.synchronize(dev)
     dev_ms = sum(a.elapsed_time(b) for a, b in evs)
     kernel_share = kern_ms / max(dev_ms, 1e-9)
@@ -534,7 +535,8 @@ def run_b200(args):
         achieved = alg_bytes / (k_ms * 1e-3) / 1e9
         ncu, ncu_status = _ncu(args.workload)
         us_iter = k_ms * 1e3 / max(it, 1)
-        floor_iter = pr["grid_barrier_us"] + item_us
+        bar_per_it = barriers / max(iters, 1)
+        floor_iter = bar_per_it * pr["grid_barrier_us"] + item_us
         roof = {"bound": "latency", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 5),
                 "traffic": ncu.get("dram_bytes") if ncu else None, "traffic_status": ncu_status,
@@ -547,6 +549,7 @@ def run_b200(args):
                 # batch work item), both measured in this run
                 "latency": {"iterations": round(it, 1), "us_per_iteration": round(us_iter, 3),
                             "grid_barrier_us": round(pr["grid_barrier_us"], 3),
+                            "grid_barriers_per_iteration": round(bar_per_it, 3),
                             "mean_item_us": round(item_us, 3),
                             "floor_us_per_iteration": round(floor_iter, 3),
                             "frac": round(floor_iter / us_iter, 4)},

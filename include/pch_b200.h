@@ -127,6 +127,8 @@ typedef struct pch_stats {
     int64_t pool_restarts;    /* ... of which reran the solve from scratch (a
                                  hard overflow); the live solver grows at an
                                  iteration boundary and continues */
+    int64_t grid_barriers;    /* grid-wide barriers the one-barrier solver ran
+                                 (fewer than iterations: CTA-local iterations) */
     double time_total_ms;     /* device time of the solve (CUDA events) */
     double time_kernel_ms;    /* persistent-kernel time only */
     /* RunStats.time_select / _propagate / _compact / _events

@@ -47,7 +47,7 @@ STAT_FIELDS = ("iterations", "windows_propagated", "total_windows_created",
                "pruned_tiny", "pruned_degenerate", "pruned_duplicate",
                "pruned_recheck", "windows_stored", "max_children_per_window",
                "events_created", "events_applied", "peak_active_pool",
-               "fans_emitted", "buffer_regrows", "pool_restarts")
+               "fans_emitted", "buffer_regrows", "pool_restarts", "grid_barriers")
 
 
 TIME_FIELDS = ("time_total_ms", "time_kernel_ms", "time_select_ms",

@@ -50,7 +50,7 @@ using namespace pch;
 enum { // the eight hot counters first: packed per thread (LocalStats)
        ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_RECHECK, ST_STORED,
        ST_EV_CREATED, ST_EV_APPLIED, ST_N_PACKED,
-       ST_PRUNE_TINY = ST_N_PACKED, ST_PRUNE_DEGEN, ST_FANS, ST_PRUNE_DUP, ST_MAXCHILD, ST_PEAK,
+       ST_PRUNE_TINY = ST_N_PACKED, ST_PRUNE_DEGEN, ST_FANS, ST_PRUNE_DUP, ST_BARRIERS, ST_MAXCHILD, ST_PEAK,
        // PCH_PROFILE section clocks (clock64 deltas summed over threads)
        ST_CYC_PROP, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
        ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES,
@@ -1795,7 +1795,10 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             // after a global iteration the other CTAs may still be reading
             // this CTA's chunks (the distributed inputs): a grid barrier
             // before it writes its parity buffers again
-            if (!local) grid_barrier<false>(ctrl, gen, [] {});
+            if (!local) {
+                grid_barrier<false>(ctrl, gen, [] {});
+                if (b == 0 && threadIdx.x == 0) s_st[ST_BARRIERS] += 1ull;
+            }
             __syncthreads();  // s_loc and this CTA's outputs are visible to its warps
             // prefix tables with only this CTA's chunk filled: the chunk
             // lookup then maps item i to slot b * ch + i unchanged
@@ -1815,6 +1818,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         // the __syncthreads before the publish already ordered every
         // thread's outputs before thread 0's release
         grid_barrier<false>(ctrl, gen, [] {});
+        if (b == 0 && threadIdx.x == 0) s_st[ST_BARRIERS] += 1ull;
         // the next iteration's inputs: S_{i+1}, P_{i+1} (parity par^1) and
         // the fan candidates of iteration i (parity par); the counts and
         // the controller's inputs are read in one round trip
@@ -2386,6 +2390,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             stats->fans_emitted += c.st[ST_FANS];
             stats->buffer_regrows += regrows;
             stats->pool_restarts += restarts;
+            stats->grid_barriers += c.st[ST_BARRIERS];
             stats->time_total_ms += t_all;
             stats->time_kernel_ms += t_k;
             // phase shares of the kernel time from the warp-cycle attribution

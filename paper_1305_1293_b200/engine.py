@@ -160,6 +160,7 @@ class RunStats:
     fans_emitted: int = 0
     buffer_regrows: int = 0
     pool_restarts: int = 0
+    grid_barriers: int = 0
     time_total: float = 0.0
     time_select: float = 0.0
     time_propagate: float = 0.0

@@ -40,9 +40,9 @@ def test_library_loads_and_reports_abi():
 
 
 def test_struct_layouts_match_header():
-    # pch_config: 8+4+4+8+8+8+4+4+8+8 ; pch_stats: 18 int64 + 7 doubles
+    # pch_config: 8+4+4+8+8+8+4+4+8+8 ; pch_stats: 19 int64 + 7 doubles
     assert ctypes.sizeof(_native.PchConfig) == 64
-    assert ctypes.sizeof(_native.PchStats) == 8 * 25
+    assert ctypes.sizeof(_native.PchStats) == 8 * 26
 
 
 def test_sass_is_sm100a():

@@ -606,7 +606,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", default="terrain1m",
-                    choices=("terrain1m", "icosphere20k", "knot4m", "sphere16m", "torus500k"))
+                    choices=("terrain1m", "icosphere20k", "knot4m", "knotg4m", "sphere16m", "torus500k"))
     ap.add_argument("--k", type=int, default=16384)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget-s", type=float, default=150.0)

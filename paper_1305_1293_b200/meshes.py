@@ -10,7 +10,9 @@ seconds:
 
 * ``terrain``        — noisy heightfield grid (config 1, ~1M faces)
 * ``torus_knot_tube``— tube swept along a (p, q) torus knot with skinny,
-                       anisotropic triangles (config 2, ~4M faces)
+                       anisotropic triangles (~4M faces, genus 1)
+* ``torus_knot_tube_handles`` — the same tube with bridges between its
+                       strands: genus 7 (config 2 as stated, "high-genus")
 * ``perturbed_sphere``— subdivided cube-sphere with radial noise
                        (config 3, ~16M faces)
 
@@ -283,6 +285,117 @@ def torus_knot_tube(p_wind: int = 2, q_wind: int = 3, n_along: int = 20000,
     return normalize_edge_scale(pts.reshape(-1, 3), _wrapped_grid_faces(n_along, n_around))
 
 
+def torus_knot_tube_handles(p_wind: int = 2, q_wind: int = 3, n_along: int = 20000,
+                            n_around: int = 100, tube: float = 0.12, handles: int = 6,
+                            hole_around: int = 6, bridge_rings: int = 24):
+    """``torus_knot_tube`` with ``handles`` bridges between strands where
+    the knot passes close to itself: genus 1 + handles.  At each site a
+    block of tube faces facing the other strand is removed on both strands
+    and the two boundary loops are joined by a straight cylinder of
+    ``bridge_rings`` rings (only edge lengths matter to the solver, so the
+    embedding need not be free of intersections).  The tube keeps its
+    skinny, anisotropic triangles; the bridges add long thin ones."""
+    t = 2.0 * np.pi * np.arange(n_along) / n_along
+
+    def curve(tt):
+        r = 2.0 + np.cos(q_wind * tt)
+        return np.column_stack([r * np.cos(p_wind * tt), r * np.sin(p_wind * tt),
+                                -np.sin(q_wind * tt)])
+
+    c = curve(t)
+    tan = curve(t + 1e-4) - curve(t - 1e-4)
+    tan /= np.linalg.norm(tan, axis=1, keepdims=True)
+    nrm = np.cross(tan, np.array([0.0, 0.0, 1.0]))
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    bin_ = np.cross(tan, nrm)
+    a = 2.0 * np.pi * np.arange(n_around) / n_around
+    wob = 1.0 + 0.15 * np.sin(7.0 * t)[:, None] * np.cos(3.0 * a)[None, :]
+    pts = (c[:, None, :] + tube * wob[..., None]
+           * (np.cos(a)[None, :, None] * nrm[:, None, :] + np.sin(a)[None, :, None] * bin_[:, None, :]))
+    # closest approaches of the knot to itself (at least a tenth of the
+    # curve apart): local minima of the nearest-strand distance
+    m = 2048
+    ci = (np.arange(m) * n_along) // m
+    cs = c[ci]
+    dist = np.linalg.norm(cs[:, None, :] - cs[None, :, :], axis=2)
+    sep = np.abs(np.arange(m)[:, None] - np.arange(m)[None, :])
+    sep = np.minimum(sep, m - sep)
+    dist[sep < m // 10] = np.inf
+    nearest = dist.min(axis=1)
+    partner = dist.argmin(axis=1)
+    minima = [k for k in range(m) if nearest[k] <= nearest[k - 1] and nearest[k] <= nearest[(k + 1) % m]]
+    sites, used = [], np.zeros(m, dtype=bool)
+    for k in sorted(minima, key=lambda k: nearest[k]):
+        if len(sites) == handles:
+            break
+        kb = int(partner[k])
+        if used[k] or used[kb]:
+            continue
+        for q in (k, kb):
+            used[np.arange(q - m // 40, q + m // 40) % m] = True
+        sites.append((int(ci[k]), int(ci[kb])))
+    # hole size: about square on the tube (along cells are shorter)
+    cell_along = np.linalg.norm(c[1] - c[0])
+    cell_around = 2.0 * np.pi * tube / n_around
+    hole_along = max(2, int(round(hole_around * cell_around / cell_along)))
+    removed = np.zeros((n_along, n_around), dtype=bool)  # quad (i, j) removed
+    loops = []
+
+    def facing(i, target):
+        d = target - c[i]
+        ang = np.arctan2(d @ bin_[i], d @ nrm[i])
+        return int(round(ang / (2.0 * np.pi) * n_around)) % n_around
+
+    for ia, ib in sites:
+        pair = []
+        for i_c, other in ((ia, ib), (ib, ia)):
+            j_c = facing(i_c, c[other])
+            i0, j0 = i_c - hole_along // 2, j_c - hole_around // 2
+            for di in range(hole_along):
+                for dj in range(hole_around):
+                    removed[(i0 + di) % n_along, (j0 + dj) % n_around] = True
+            # boundary loop of the hole, counterclockwise in (i, j)
+            loop = ([((i0 + k) % n_along, j0 % n_around) for k in range(hole_along)]
+                    + [((i0 + hole_along) % n_along, (j0 + k) % n_around) for k in range(hole_around)]
+                    + [((i0 + hole_along - k) % n_along, (j0 + hole_around) % n_around)
+                       for k in range(hole_along)]
+                    + [(i0 % n_along, (j0 + hole_around - k) % n_around) for k in range(hole_around)])
+            pair.append([i * n_around + j for i, j in loop])
+        loops.append(pair)
+    faces = _wrapped_grid_faces(n_along, n_around)
+    keep = ~np.repeat(removed.ravel(), 2)
+    faces = [faces[keep]]
+    positions = [pts.reshape(-1, 3)]
+    nv = n_along * n_around
+    for la, lb in loops:
+        la = np.asarray(la)
+        # loop B runs the other way round (the bridge enters the other tube
+        # from outside); start it at the vertex nearest loop A's first
+        lb = np.asarray(lb)[::-1]
+        pa, pb = positions[0][la], positions[0][lb]
+        sh = int(np.argmin(np.linalg.norm(pb - pa[0], axis=1)))
+        lb, pb = np.roll(lb, -sh), np.roll(pb, -sh, axis=0)
+        n = len(la)
+        rings = [la]
+        for k in range(1, bridge_rings):
+            f = k / bridge_rings
+            positions.append(pa + f * (pb - pa))
+            rings.append(np.arange(nv, nv + n))
+            nv += n
+        rings.append(lb)
+        for r0, r1 in zip(rings[:-1], rings[1:]):
+            nx = np.roll(np.arange(n), -1)
+            # orientation opposite to the holes' boundary half-edges
+            faces.append(np.stack([r0, r0[nx], r1[nx]], 1))
+            faces.append(np.stack([r0, r1[nx], r1], 1))
+    faces = np.vstack(faces)
+    # drop the vertices inside the holes (no face left)
+    used = np.zeros(nv, dtype=bool)
+    used[faces.ravel()] = True
+    remap = np.cumsum(used) - 1
+    return normalize_edge_scale(np.vstack(positions)[used], remap[faces])
+
+
 def perturbed_sphere(n: int = 1155, amplitude: float = 0.04, seed: int = 1293):
     """Cube-sphere: each cube face split into ``n x n`` quads (two
     triangles each; n=1155 gives 16,008,300 faces), projected to the unit
@@ -379,6 +492,10 @@ def bench_mesh(name: str) -> SurfaceMesh:
         return build_half_edge_mesh(*torus_knot_tube())
     if name == "knot1m":  # configs[2] at a quarter of the size: the oracle's full-fan mode fits
         return build_half_edge_mesh(*torus_knot_tube(n_along=10000, n_around=50))
+    if name == "knotg4m":  # configs[2] as stated: a high-genus (7) torus-knot tube, 4M faces
+        return build_half_edge_mesh(*torus_knot_tube_handles())
+    if name == "knotg1m":  # ... at a quarter of the size (full-fan oracle fits)
+        return build_half_edge_mesh(*torus_knot_tube_handles(n_along=10000, n_around=50))
     if name == "sphere16m":
         return build_half_edge_mesh(*perturbed_sphere(1155))
     if name == "torus500k":

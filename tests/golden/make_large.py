@@ -54,7 +54,9 @@ def cases():
            ("torus500k", "torus500k", "centre"),
            ("sphere16m", "sphere16m", "centre"),
            ("knot4m", "knot4m", 0),
-           ("knot1m", "knot1m", 0)]
+           ("knot1m", "knot1m", 0),
+           ("knotg1m", "knotg1m", 0),
+           ("knotg4m", "knotg4m", 0)]
     out += [(f"torus500k_row{i}", "torus500k", s) for i, s in enumerate(TORUS_ROW_SOURCES)]
     return out
 

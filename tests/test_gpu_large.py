@@ -111,18 +111,21 @@ def test_config_single_source(case, deterministic):
     print(case, "det" if deterministic else "live", rep, f"{st.time_kernel_ms:.2f} ms")
 
 
+@pytest.mark.parametrize("case", ["knot1m", "knotg1m"])
 @pytest.mark.parametrize("mode", ["default", "deterministic_margin"])
-def test_config_knot1m(mode):
+def test_config_knot1m(case, mode):
     """configs[2] at a quarter size (1M-face torus knot, same skinny tube):
     small enough for the oracle's full-fan mode, so the strict rule holds
     against the reference answer.  The reference's default mode leaves
-    rounding holes and detoured vertices here too."""
+    rounding holes and detoured vertices here too.  knotg1m: the same tube
+    with six bridges between its strands (genus 7, configs[2]'s
+    "high-genus")."""
     from paper_1305_1293_b200 import EngineConfig, run_pch
-    m, g = _fixture("knot1m")
+    m, g = _fixture(case)
     cfg = EngineConfig() if mode == "default" else EngineConfig(deterministic=True, fan_margin=1e-5)
     d, st = run_pch(m, [int(g["source"])], cfg)
-    rep = check_field(m, d, g, f"knot1m {mode}")
-    print("knot1m", mode, {k: (v if not isinstance(v, list) else len(v)) for k, v in rep.items()},
+    rep = check_field(m, d, g, f"{case} {mode}")
+    print(case, mode, {k: (v if not isinstance(v, list) else len(v)) for k, v in rep.items()},
           f"{st.time_kernel_ms:.1f} ms")
 
 
@@ -167,16 +170,17 @@ def _knot4m_report(m, d, g):
             "below_euclid": int(np.sum(d[fin] < chord[fin] * (1 - 1e-12) - 1e-9))}
 
 
-def test_config_knot4m_exact():
+@pytest.mark.parametrize("case", ["knot4m", "knotg4m"])
+def test_config_knot4m_exact(case):
     """configs[2], the 4M-face torus knot, in the configuration exact on it
     (two-barrier solver, 1e-4 rad fan margin; 27 s): every vertex
     reached, never longer than the reference on any sampled vertex, shorter
     only on the few the reference detoured, edge-Lipschitz everywhere."""
     from paper_1305_1293_b200 import EngineConfig, run_pch
-    m, g = _fixture("knot4m")
+    m, g = _fixture(case)
     d, st = run_pch(m, [int(g["source"])], EngineConfig(deterministic=True, fan_margin=1e-4))
     r = _knot4m_report(m, d, g)
-    print("knot4m exact", {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()},
+    print(case, "exact", {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()},
           f"{st.time_kernel_ms:.1f} ms")
     assert r["source_zero"] and r["below_euclid"] == 0
     assert r["holes_gpu"] == 0
@@ -185,8 +189,9 @@ def test_config_knot4m_exact():
     assert not r["lipschitz_vertices"]
 
 
+@pytest.mark.parametrize("case", ["knot4m", "knotg4m"])
 @pytest.mark.parametrize("fan_mode", ["clip", "full_edges"])
-def test_config_knot4m_live_residual(fan_mode):
+def test_config_knot4m_live_residual(case, fan_mode):
     """configs[2] with the fast one-barrier solver: the residual it leaves
     on this ill-conditioned mesh, bounded (measured over
     repeated runs, the solver is not bitwise reproducible).  Default (fan
@@ -195,10 +200,10 @@ def test_config_knot4m_live_residual(fan_mode):
     7824 unreached and >= 530 detoured.  full_edges: none unreached, 0-2
     detoured vertices."""
     from paper_1305_1293_b200 import EngineConfig, run_pch
-    m, g = _fixture("knot4m")
+    m, g = _fixture(case)
     d, st = run_pch(m, [int(g["source"])], EngineConfig(fan_mode=fan_mode))
     r = _knot4m_report(m, d, g)
-    print("knot4m live", fan_mode, {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()},
+    print(case, "live", fan_mode, {k: (v if not isinstance(v, list) else len(v)) for k, v in r.items()},
           f"{st.time_kernel_ms:.1f} ms")
     assert r["source_zero"] and r["below_euclid"] == 0
     if fan_mode == "clip":

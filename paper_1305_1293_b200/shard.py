@@ -31,7 +31,8 @@ def gather_rows(local, n_total: int, rank: int, world: int):
     the original source order.  ``local`` is a ``[len(shard), n_vertices]``
     float64 torch tensor on this rank's device (NCCL) or on the CPU (gloo);
     rank 0 returns the ``[n_total, n_vertices]`` tensor on the same device,
-    the other ranks ``None``.  One collective, no host round trip."""
+    the other ranks ``None``.  One point-to-point transfer per rank into
+    rank 0, no host round trip."""
     import torch
     import torch.distributed as dist
 
@@ -42,10 +43,17 @@ def gather_rows(local, n_total: int, rank: int, world: int):
         pad = torch.full((cmax - local.shape[0], nv), float("nan"), dtype=local.dtype,
                          device=local.device)
         local = torch.cat([local, pad])
-    bufs = [torch.empty_like(local) for _ in range(world)] if rank == 0 else None
-    dist.gather(local.contiguous(), bufs, dst=0)
+    # point-to-point into rank 0 (NCCL send/recv over NVLink; gloo on CPU),
+    # all transfers posted at once
+    local = local.contiguous()
     if rank != 0:
+        for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, local, 0)]):
+            w.wait()
         return None
+    bufs = [local] + [torch.empty_like(local) for _ in range(1, world)]
+    ops = [dist.P2POp(dist.irecv, bufs[r], r) for r in range(1, world)]
+    for w in dist.batch_isend_irecv(ops):
+        w.wait()
     out = torch.empty((n_total, nv), dtype=local.dtype, device=local.device)
     for r in range(world):
         idx = torch.as_tensor(shard_sources(range(n_total), r, world), device=local.device)

@@ -881,15 +881,11 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     ls.add(ST_PRUNE_DEGEN, degen + (ml && fl == CH_DEGEN ? 1u : 0u) + (mr && frr == CH_DEGEN ? 1u : 0u));
     ls.add(ST_PRUNE_TINY, (ml && fl == CH_TINY ? 1u : 0u) + (mr && frr == CH_TINY ? 1u : 0u));
     ls.add(ST_PRUNE_ICH, (ml && fl == CH_ICH ? 1u : 0u) + (mr && frr == CH_ICH ? 1u : 0u));
-    if (sl) {
-        out0 = cl;
-        nc = 1;
-    }
-    if (sr) {
-        if (nc) out1 = cr;
-        else out0 = cr;
-        ++nc;
-    }
+    // compacted children: the right one is always out1 when both are
+    // kept, so only out0 needs a select (not two predicated copies)
+    out0 = sl ? cl : cr;
+    out1 = cr;
+    nc = (sl ? 1 : 0) + (sr ? 1 : 0);
 
     // ---- events, issued together (order independent: min / CAS-min) ----
     if (ev0) dist_event(p, T, sg, v0, cand0, ls);

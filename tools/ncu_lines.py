@@ -24,9 +24,9 @@ def sass_lines(lib, kernel):
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", lib], cwd=tmp, check=True,
                    capture_output=True)
-    cub = [f for f in os.listdir(tmp) if f.endswith(".cubin")][0]
-    dis = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, cub)],
-                         capture_output=True, text=True).stdout
+    dis = "\n".join(subprocess.run(["nvdisasm", "-g", "-c", os.path.join(tmp, c)],
+                                   capture_output=True, text=True).stdout
+                    for c in sorted(os.listdir(tmp)) if c.endswith(".cubin"))
     out, cur_fn, cur_line = {}, None, None
     for l in dis.splitlines():
         m = re.match(r"\s*\.text\.(\S+):", l)

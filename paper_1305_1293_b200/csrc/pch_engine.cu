@@ -47,10 +47,10 @@ using namespace pch;
 // ---------------------------------------------------------------------------
 // device state
 
-enum { // the eight hot counters first: packed per thread (LocalStats)
+enum { // the ten hot counters first: packed per thread (LocalStats)
        ST_PROPAGATED, ST_CREATED, ST_PRUNE_ICH, ST_PRUNE_SPLIT, ST_RECHECK, ST_STORED,
-       ST_EV_CREATED, ST_EV_APPLIED, ST_N_PACKED,
-       ST_PRUNE_TINY = ST_N_PACKED, ST_PRUNE_DEGEN, ST_FANS, ST_PRUNE_DUP, ST_BARRIERS, ST_MAXCHILD, ST_PEAK,
+       ST_EV_CREATED, ST_EV_APPLIED, ST_PRUNE_TINY, ST_PRUNE_DEGEN, ST_N_PACKED,
+       ST_FANS = ST_N_PACKED, ST_PRUNE_DUP, ST_BARRIERS, ST_MAXCHILD, ST_PEAK,
        // PCH_PROFILE section clocks (clock64 deltas summed over threads)
        ST_CYC_PROP, ST_CYC_POOL, ST_CYC_FANSPAN, ST_CYC_FANITEM,
        ST_CYC_PART, ST_N_POOL, ST_N_PART, ST_N_FANITEM, ST_CAS_ANGLE_CALLS, ST_CAS_ANGLE_TRIES, ST_CAS_FAN_CALLS, ST_CAS_FAN_TRIES,
@@ -119,6 +119,7 @@ struct Params {
     long long K;
     double eps_win;
     double inv_r0;             // 1 / radius of the angular tiny-window rule (huge: absolute)
+    double eps_win2, inv_r02;  // their squares (make_child compares squared)
     double fan_widen;          // saddle-fan interval widened by this angle on both sides
     int phase;                 // attribute cycles to the four phases (PCH_FLAG_PHASE_TIMES)
     int resume;                // live solver: continue at ctrl->res_it after a pool growth
@@ -301,26 +302,30 @@ __device__ __forceinline__ Win load_win(const WinSoA &W, unsigned long long i) {
     return c;
 }
 
-// Run counters.  The eight hot ones (ST_PROPAGATED .. ST_EV_APPLIED) are
-// packed as 16-bit fields into two per-thread registers and folded into
+// Run counters.  The ten hot ones (ST_PROPAGATED .. ST_PRUNE_DEGEN) are
+// packed as 16-bit fields into three per-thread registers and folded into
 // the CTA's shared counters when any field passes 2^15 and at exit (one
 // warp reduction per field, one shared atomic per nonzero field from lane
 // 0): a shared-memory atomic per increment serialises the propagation path
 // (measured ~25% of the solve).  A trip adds at most 4 per chained
 // propagation (3 distance + 1 angle event) to a field, far below the 2^15
 // headroom, so a fold is needed only every few thousand trips -- folding
-// on a fixed short period had cost 0.24 ms of the 1M-face field.  The rare
-// ones (tiny / degenerate prunes, fans), profiling clocks, maxima and
-// `direct` objects go straight to shared memory, only when nonzero.
+// on a fixed short period had cost 0.24 ms of the 1M-face field.  The
+// tiny / degenerate prunes are packed too (as shared atomics under a branch
+// they cost every crossing a divergent region); the rare ones (fans, dup
+// prunes), profiling clocks, maxima and `direct` objects go straight to
+// shared memory, only when nonzero.
 struct LocalStats {
     unsigned long long *s;
     bool direct;
-    unsigned long long a = 0ull, b = 0ull;
+    unsigned long long a = 0ull, b = 0ull, c = 0ull;
     __device__ __forceinline__ void add(int i, unsigned long long x = 1ull) {
         if (!direct && i <= 3) {
             a += x << (16 * i);
-        } else if (!direct && i < ST_N_PACKED) {
+        } else if (!direct && i <= 7) {
             b += x << (16 * (i - 4));
+        } else if (!direct && i < ST_N_PACKED) {
+            c += x << (16 * (i - 8));
         } else if (x) {
             atomicAdd(s + i, x);
         }
@@ -328,7 +333,7 @@ struct LocalStats {
     __device__ __forceinline__ void max(int i, unsigned long long x) { atomicMax(s + i, x); }
     // some lane of the (converged) warp is past half of a field's range
     __device__ __forceinline__ bool fold_due() const {
-        return __any_sync(0xffffffffu, ((a | b) & 0x8000800080008000ull) != 0ull);
+        return __any_sync(0xffffffffu, ((a | b | c) & 0x8000800080008000ull) != 0ull);
     }
     // fold the packed fields into shared memory (whole warp, converged):
     // one warp reduction per field, lane 0 adds the nonzero sums
@@ -336,11 +341,11 @@ struct LocalStats {
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int k = 0; k < ST_N_PACKED; ++k) {
-            const unsigned long long w = k <= 3 ? a : b;
+            const unsigned long long w = k <= 3 ? a : k <= 7 ? b : c;
             const unsigned int f = __reduce_add_sync(0xffffffffu, (unsigned int)((w >> (16 * (k & 3))) & 0xffffull));
             if (lane == 0 && f) atomicAdd(s + k, (unsigned long long)f);
         }
-        a = b = 0ull;
+        a = b = c = 0ull;
     }
 };
 
@@ -721,7 +726,7 @@ __device__ __forceinline__ void fan_item(const Params &p, const RowTabs &t, uint
     Win c;
     int fate = make_child(__ldg(&fr.che), __ldg(&fr.cho), cv0, cv1, __ldg(&fr.capx), __ldg(&fr.lc), px, py,
                           qx, qy, s0, s1, 0.0, 0.0, cand,
-                          gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win, p.inv_r0, c);
+                          gp, gq, INFINITY, 0.0, 0.0, true, p.eps_win2, p.inv_r02, c);
     c.row = row;
     if (fate == CH_STORED) {
         if (epoch && p.dup_tab && fan_duplicate(p, c, epoch)) {
@@ -854,10 +859,10 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     Win cl, cr;
     const int fl = make_child(3 * (fr / 3) + a1, cho_l, v0f, vdf, apx_l, lan, 0.0, 0.0, dx, dy, rA,
                               occ ? 1.0 : rB,
-                              ix, iy, dps, g0, gdd, g1, ell, 0.0, true, p.eps_win, p.inv_r0, cl);
+                              ix, iy, dps, g0, gdd, g1, ell, 0.0, true, p.eps_win2, p.inv_r02, cl);
     const int frr = make_child(3 * (fr / 3) + a2, cho_r, vdf, v1f, apx_r, lpv, dx, dy, ell, 0.0,
                                occ ? 0.0 : rA, rB,
-                               ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win, p.inv_r0, cr);
+                               ix, iy, dps, gdd, g1, g0, 0.0, 0.0, false, p.eps_win2, p.inv_r02, cr);
     cl.row = cr.row = w.row;
     // one-angle-one-split (Fig. 4a): a stored window that already gives
     // the apex a shorter distance leaves only the child on our side
@@ -2182,6 +2187,8 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.inv_r0 = (cfg->flags & PCH_FLAG_ABSOLUTE_TINY) ? 1e300 : 1.0 / (TINY_R0_EDGES * m->mean_edge);
         if (const char *r0 = getenv("PCH_TINY_R0"))  // development: radius in mean edges
             if (!(cfg->flags & PCH_FLAG_ABSOLUTE_TINY)) p.inv_r0 = 1.0 / (atof(r0) * m->mean_edge);
+        p.eps_win2 = p.eps_win * p.eps_win;
+        p.inv_r02 = p.inv_r0 * p.inv_r0;
         p.fan_widen = cfg->fan_margin;
         // one grid barrier every LOCAL_ITERS iterations, the others CTA-local
         // (measured: terrain1m 7.64 -> 7.06 ms, sphere16m 112 -> 102 ms;

@@ -23,6 +23,25 @@ __global__ void k_fp(double *out, long long *cyc, double x0, int n) {
     cyc[3] = (t4 - t3) / n; cyc[4] = (t5 - t4) / n; cyc[5] = (t6 - t5) / n;
 }
 
+__global__ void k_fp2(double *out, long long *cyc, double x0, int n) {
+    double x = x0;
+    long long t0 = clock64();
+    for (int i = 0; i < n; ++i) x = x * 1.0000001;  // dmul
+    long long t1 = clock64();
+    for (int i = 0; i < n; ++i) x = x + 1e-9;  // dadd
+    long long t2 = clock64();
+    for (int i = 0; i < n; ++i) x = (x > 0.5 ? x : x + 1.0) * 0.999;  // dsetp + fsel + dmul
+    long long t3 = clock64();
+    for (int i = 0; i < n; ++i) {
+        double r;
+        asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+        x = r + 1e-3;
+    }  // mufu rcp64h + dadd
+    long long t4 = clock64();
+    out[1] = x;
+    cyc[8] = (t1 - t0) / n; cyc[9] = (t2 - t1) / n; cyc[10] = (t3 - t2) / n; cyc[11] = (t4 - t3) / n;
+}
+
 __global__ void k_chase(const int *next, long long *cyc, int *sink, int n, int start) {
     int j = start;
     long long t0 = clock64();
@@ -51,6 +70,10 @@ int main() {
     long long h[8];
     cudaMemcpy(h, cyc, 64, cudaMemcpyDeviceToHost);
     printf("dfma %lld  sqrt %lld  rcp-div %lld  atan2 %lld  sincos %lld  mul+add %lld cycles\n", h[0], h[1], h[2], h[3], h[4], h[5]);
+    k_fp2<<<1, 1>>>(out, cyc, 0.7, 1000);
+    long long h2[16];
+    cudaMemcpy(h2, cyc, 128, cudaMemcpyDeviceToHost);
+    printf("dmul %lld  dadd %lld  dsetp+fsel+dmul %lld  rcp.approx+dadd %lld cycles\n", h2[8], h2[9], h2[10], h2[11]);
     // pointer chase: small (L1/L2) and large (HBM) footprints
     for (long long elems : {1LL << 10, 1LL << 20, 1LL << 24, 1LL << 27}) {
         int *hn = new int[elems];

@@ -1530,8 +1530,11 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         if (!local && nS > 0 && it > 0 && smax < t) t = smax;
         if (!local && nS == 0 && pmin > t && pmin < INFINITY) t = pmin;
         const double tn = t + delta;  // threshold of S_{i+1}
-        const WinSoA Sc = par ? p.S2 : p.S, Sn = par ? p.S : p.S2;
-        const WinSoA Pc = par ? p.Y : p.X, Pn = par ? p.X : p.Y;
+        // the iteration's sets as regions of p.S's columns (alloc_soa4):
+        // batch in / out, pool in / out
+        // (region numbers: batch in = par, batch out = par ^ 1, pool in =
+        // 2 + par, pool out = 2 + (par ^ 1); offsets formed at the use)
+        const unsigned int rSc = (unsigned int)par, rPc = 2u + (unsigned int)par;
         const FanEv *fev = p.fanev[par ^ 1];        // fan candidates of iteration i-1
         FanEv *fout = p.fanev[par] + (size_t)b * chF;  // this CTA's chunk for iteration i
         if (!local && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1558,7 +1561,10 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         };
         // one window into this CTA's chunk of S_{i+1} / P_{i+1}
         auto put_at = [&](bool sel, unsigned int k, const Win &c) {
-            if (k < ch) store_win(sel ? Sn : Pn, (unsigned long long)b * ch + k, c);
+            if (k < ch)
+                store_win(p.S, (unsigned long long)((sel ? 0u : 2u) + (unsigned int)(par ^ 1)) * (unsigned long long)p.cap +
+                                   (unsigned long long)b * ch + k,
+                          c);
             else atomicExch(&ctrl->error, ERR_OVERFLOW);
         };
         // rare paths (divergent): one shared atomic per window
@@ -1603,7 +1609,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                         asm volatile("" ::"l"(slot0));
                         trace_max_warp(p, it, TR_TRIP0);
                     }
-                    Win win = load_win(Sc, slot0);
+                    Win win = load_win(p.S, (unsigned long long)rSc * (unsigned long long)p.cap + slot0);
                     if (p.trace) {
                         asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
                         trace_max_warp(p, it, TR_LOADED);
@@ -1691,7 +1697,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             } else {
                 const unsigned int i = ((wi - nwS - nwF) << 5) + lane;
                 if (i < nP) {
-                    o0 = load_win(Pc, chunk_slot(s_pre[1], G, i, ch));
+                    o0 = load_win(p.S, (unsigned long long)rPc * (unsigned long long)p.cap + chunk_slot(s_pre[1], G, i, ch));
                     no = 1;
                 }
             }
@@ -2044,16 +2050,33 @@ static int ws_alloc(pch_mesh *m, T **out, size_t count) {
     return PCH_OK;
 }
 
-static int alloc_soa(pch_mesh *m, WinSoA &W, long long cap) {
+// The four window sets share each column's allocation: region r of a
+// column starts at r * cap (S = 0, S2 = 1, X = 2, Y = 3), so the one-barrier
+// solver addresses every set through p.S's pointers plus a region offset --
+// no per-window select between two sets' eight column pointers.
+static int alloc_soa4(pch_mesh *m, Params &p, long long cap) {
     int rc;
-    if ((rc = ws_alloc(m, &W.hv, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.vr, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.b0, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.b1, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.d0, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.d1, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.d, cap))) return rc;
-    if ((rc = ws_alloc(m, &W.key, cap))) return rc;
+    WinSoA &W = p.S;
+    if ((rc = ws_alloc(m, &W.hv, 4 * cap))) return rc;
+    if ((rc = ws_alloc(m, &W.vr, 4 * cap))) return rc;
+    if ((rc = ws_alloc(m, &W.b0, 4 * cap))) return rc;
+    if ((rc = ws_alloc(m, &W.b1, 4 * cap))) return rc;
+    if ((rc = ws_alloc(m, &W.d0, 4 * cap))) return rc;
+    if ((rc = ws_alloc(m, &W.d1, 4 * cap))) return rc;
+    if ((rc = ws_alloc(m, &W.d, 4 * cap))) return rc;
+    if ((rc = ws_alloc(m, &W.key, 4 * cap))) return rc;
+    WinSoA *sets[3] = {&p.S2, &p.X, &p.Y};
+    for (int r = 1; r < 4; ++r) {
+        WinSoA &R = *sets[r - 1];
+        R.hv = W.hv + r * cap;
+        R.vr = W.vr + r * cap;
+        R.b0 = W.b0 + r * cap;
+        R.b1 = W.b1 + r * cap;
+        R.d0 = W.d0 + r * cap;
+        R.d1 = W.d1 + r * cap;
+        R.d = W.d + r * cap;
+        R.key = W.key + r * cap;
+    }
     return PCH_OK;
 }
 
@@ -2091,10 +2114,7 @@ static int ensure_ws(pch_mesh *m, long long cap, int rows, bool exact = false) {
     if ((rc = ws_alloc(m, &p.fanev[0], p.fancap))) return rc;
     if ((rc = ws_alloc(m, &p.fanev[1], p.fancap))) return rc;
     if ((rc = ws_alloc(m, &p.fanev[2], p.fancap))) return rc;
-    if ((rc = alloc_soa(m, p.X, cap))) return rc;
-    if ((rc = alloc_soa(m, p.Y, cap))) return rc;
-    if ((rc = alloc_soa(m, p.S, cap))) return rc;
-    if ((rc = alloc_soa(m, p.S2, cap))) return rc;
+    if ((rc = alloc_soa4(m, p, cap))) return rc;
     if ((rc = ws_alloc(m, &p.hist[0], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.hist[1], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.hist2[0], NBINS + 1))) return rc;
@@ -2114,17 +2134,13 @@ static int grow_ws(pch_mesh *m, long long cap, int par, cudaStream_t st) {
     Params &p = m->prm;
     const int G = m->grid_live;
     const long long old_cap = p.cap, old_fancap = p.fancap;
-    std::vector<void *> old = {p.X.hv, p.X.vr, p.X.b0, p.X.b1, p.X.d0, p.X.d1, p.X.d, p.X.key,
-                               p.Y.hv, p.Y.vr, p.Y.b0, p.Y.b1, p.Y.d0, p.Y.d1, p.Y.d, p.Y.key,
-                               p.S.hv, p.S.vr, p.S.b0, p.S.b1, p.S.d0, p.S.d1, p.S.d, p.S.key,
-                               p.S2.hv, p.S2.vr, p.S2.b0, p.S2.b1, p.S2.d0, p.S2.d1, p.S2.d, p.S2.key,
+    // (the four window sets live in p.S's column allocations)
+    std::vector<void *> old = {p.S.hv, p.S.vr, p.S.b0, p.S.b1, p.S.d0, p.S.d1, p.S.d, p.S.key,
                                p.fanev[0], p.fanev[1], p.fanev[2], p.tv_list, p.te_list};
     const WinSoA oX = p.X, oY = p.Y, oS = p.S, oS2 = p.S2;
     FanEv *oF[3] = {p.fanev[0], p.fanev[1], p.fanev[2]};
     int rc;
-    if ((rc = alloc_soa(m, p.X, cap)) || (rc = alloc_soa(m, p.Y, cap)) || (rc = alloc_soa(m, p.S, cap)) ||
-        (rc = alloc_soa(m, p.S2, cap)))
-        return rc;
+    if ((rc = alloc_soa4(m, p, cap))) return rc;
     p.fancap = std::max<long long>(cap, 1 << 16);
     for (int q = 0; q < 3; ++q)
         if ((rc = ws_alloc(m, &p.fanev[q], p.fancap))) return rc;

@@ -1128,10 +1128,58 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             }
             ls.add(ST_STORED);
         };
+        // saddle fans of iteration it-1, one warp per fan event with the
+        // lanes spread over the fan's wedges.  Only the event whose candidate
+        // is the committed distance and wins the per-vertex pick (smallest
+        // candidate, then anchor / direction) emits, so each improved saddle
+        // fans out once per improvement.  Every input is frozen, so which
+        // warp runs an event (and when) does not change the outcome.
+        const unsigned long long nFc = [&] {
+            if (it == 0) return 0ull;
+            const unsigned long long nF = *(volatile unsigned long long *)&prev.nF;
+            return nF < (unsigned long long)p.fancap ? nF : (unsigned long long)p.fancap;
+        }();
+        const FanEv *fe = p.fanev[(it + 2) % 3];
+        auto fan_event_warp = [&](unsigned long long i, Win &c, unsigned int &n) {
+            long long c3 = p.prof ? clock64() : 0;
+            FanEv e = fe[i];
+            const double rel = fan_rel(e);
+            const double dv = __ldcg(p.dist_cur + e.v);
+            const ulonglong2 pk = __ldcg(p.fanpick[(it + 2) % 3] + e.v);
+            const unsigned long long lo =
+                fan_tiebreak(e);
+            FanSpan f;
+            if (__double_as_longlong(dv) == __double_as_longlong(e.cand) &&
+                pk.x == (unsigned long long)__double_as_longlong(e.cand) && pk.y == lo &&
+                fan_span(p, e.v, e.anchor, rel, false, f)) {
+                if (lane == 0) ls.add(ST_FANS);
+                const int items = f.m * f.reps;
+                if (lane < items) {
+                    fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, lane % f.m, lane / f.m, false,
+                             [&](const Win &x) { c = x; n = 1; }, ls, p.dup_epoch + it + 1u);
+                }
+                // wedges beyond the warp width (valence > 32): rare,
+                // appended with a warp-aggregated global slot
+                for (int q = lane + 32; q < items; q += 32)
+                    fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, q % f.m, q / f.m, false,
+                             [&](const Win &x) { put_pool(x, warp_alloc(&cur.nC, true)); }, ls,
+                             p.dup_epoch + it + 1u);
+            }
+            if (p.prof) {
+                ls.add(ST_CYC_FANITEM, clock64() - c3);
+                ls.add(ST_N_FANITEM);
+            }
+        };
         // (A1) the selected batch S_i: one thread per window, children into
-        // registers, pool slots reserved once per CTA and trip
+        // registers, pool slots reserved once per CTA and trip.  The warps
+        // the last trip leaves without a window run fan events meanwhile
+        // (the first nFa of them) instead of idling until A2.
+        unsigned long long nFa = 0;
         {
             const unsigned long long trips = (nS + gthreads - 1) / gthreads;
+            const unsigned long long last = trips ? nS - (trips - 1) * gthreads : 0ull;
+            const unsigned long long busyw = (last + 31) >> 5;  // warps of the last trip with windows
+            nFa = trips ? min(nFc, nwarps - busyw) : 0ull;
             for (unsigned long long t = 0; t < trips; ++t) {
                 const unsigned long long i = t * gthreads + wtid;
                 Win ca, cb;
@@ -1143,6 +1191,10 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                                    cb, ls);
                     if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
                     if (nc > maxchild) maxchild = nc;
+                } else if (t + 1 == trips && gwid >= busyw && gwid - busyw < nFa) {
+                    unsigned int n = 0;
+                    fan_event_warp(gwid - busyw, ca, n);
+                    nc = (int)n;
                 }
                 long long c2 = p.prof ? clock64() : 0;
                 const unsigned long long rel = trip_flush(p, sg, cur, it, (unsigned int)nc);
@@ -1155,50 +1207,15 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             }
         }
         phase(ST_PH_PROP);
-        // (A2) saddle fans of iteration it-1, one warp per fan event with the
-        // lanes spread over the fan's wedges.  Only the event whose candidate
-        // is the committed distance and wins the per-vertex pick (smallest
-        // candidate, then anchor / direction) emits, so each improved saddle
-        // fans out once per improvement.
-        if (it > 0) {
-            const unsigned long long nF = *(volatile unsigned long long *)&prev.nF;
-            const unsigned long long nFc = nF < (unsigned long long)p.fancap ? nF : p.fancap;
-            const FanEv *fe = p.fanev[(it + 2) % 3];
-            const unsigned long long trips = (nFc + nwarps - 1) / nwarps;
+        // (A2) the fan events the idle warps of A1 did not take
+        {
+            const unsigned long long nrest = nFc - nFa;
+            const unsigned long long trips = (nrest + nwarps - 1) / nwarps;
             for (unsigned long long t = 0; t < trips; ++t) {
-                const unsigned long long i = t * nwarps + gwid;
+                const unsigned long long i = nFa + t * nwarps + gwid;
                 Win c;
                 unsigned int n = 0;
-                if (i < nFc) {
-                    long long c3 = p.prof ? clock64() : 0;
-                    FanEv e = fe[i];
-                    const double rel = fan_rel(e);
-                    const double dv = __ldcg(p.dist_cur + e.v);
-                    const ulonglong2 pk = __ldcg(p.fanpick[(it + 2) % 3] + e.v);
-                    const unsigned long long lo =
-                        fan_tiebreak(e);
-                    FanSpan f;
-                    if (__double_as_longlong(dv) == __double_as_longlong(e.cand) &&
-                        pk.x == (unsigned long long)__double_as_longlong(e.cand) && pk.y == lo &&
-                        fan_span(p, e.v, e.anchor, rel, false, f)) {
-                        if (lane == 0) ls.add(ST_FANS);
-                        const int items = f.m * f.reps;
-                        if (lane < items) {
-                            fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, lane % f.m, lane / f.m, false,
-                                     [&](const Win &x) { c = x; n = 1; }, ls, p.dup_epoch + it + 1u);
-                        }
-                        // wedges beyond the warp width (valence > 32): rare,
-                        // appended with a warp-aggregated global slot
-                        for (int q = lane + 32; q < items; q += 32)
-                            fan_item(p, row_tabs(p, 0u, it), 0u, e.cand, f, q % f.m, q / f.m, false,
-                                     [&](const Win &x) { put_pool(x, warp_alloc(&cur.nC, true)); }, ls,
-                                     p.dup_epoch + it + 1u);
-                    }
-                    if (p.prof) {
-                        ls.add(ST_CYC_FANITEM, clock64() - c3);
-                        ls.add(ST_N_FANITEM);
-                    }
-                }
+                if (i < nFc) fan_event_warp(i, c, n);
                 unsigned long long rel = cta_alloc(&cur.nC, n);
                 if (n) put_pool(c, rel);
             }

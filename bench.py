@@ -500,11 +500,13 @@ def run_b200(args):
 
     # ---- end-to-end leg: the reference-facing call with host buffers ----
     e2e_ms = 0.0
-    for i in range(args.steps):
+    host = None
+    for i in range(args.warmup + args.steps):  # warm-up calls untimed, like the device leg
         torch.cuda.synchronize(dev)
         t = time.perf_counter()
         host, _ = run_pch(mesh, [src], cfg)
-        e2e_ms += (time.perf_counter() - t) * 1e3
+        if i >= args.warmup:
+            e2e_ms += (time.perf_counter() - t) * 1e3
     if ws > 1:
         torch.distributed.barrier()
     # the default solver reads live tables: repeated solves agree to

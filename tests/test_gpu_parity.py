@@ -340,3 +340,24 @@ def test_phase_times_reported():
     assert st.prop_item_us > 0.0
     _, st0 = run_pch(m, g["sources"])
     assert st0.time_propagate == 0.0
+
+
+def test_fields_returned_in_independent_host_buffers():
+    """run_pch hands back its field in page-locked host memory from a
+    caching allocator (engine.py _host_field): every result must stay its
+    own buffer -- a later solve, or dropping an earlier result, never
+    rewrites a field the caller still holds (views included)."""
+    _gpu()
+    from paper_1305_1293_b200 import run_pch
+    m, g = load_golden("icosphere5120_multi16")
+    a, _ = run_pch(m, [0])
+    a_copy = a.copy()
+    view = a[10:20]
+    for s in (1, 2, 3):
+        b, _ = run_pch(m, [s])
+        assert not np.shares_memory(a, b)
+        del b
+    del a
+    c, _ = run_pch(m, [4])
+    assert np.array_equal(view, a_copy[10:20])
+    assert c.dtype == np.float64 and c.shape == (m.n_vertices,) and c.flags.writeable

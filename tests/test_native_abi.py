@@ -122,3 +122,11 @@ def test_fps_no_device_raises_loudly(cube):
     from paper_1305_1293_b200 import farthest_point_sampling
     with pytest.raises(_native.NativeUnavailable):
         farthest_point_sampling(cube, 2, 0)
+
+
+def test_host_field_is_plain_numpy_without_cuda():
+    """Without a visible GPU the readback buffer is ordinary numpy memory
+    (the page-locked allocator is only plumbing for the device copy)."""
+    from paper_1305_1293_b200.engine import _host_field
+    a = _host_field(1000)
+    assert a.shape == (1000,) and a.dtype == np.float64 and a.flags.writeable

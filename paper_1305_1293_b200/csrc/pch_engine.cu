@@ -112,7 +112,7 @@ struct Params {
                                // kernel double-buffers S/S2 and P = X/Y
     long long cap;
     unsigned int *hist[2];     // NBINS + 1 bins each
-    unsigned int *hist2[2];    // exact selection: the K-th key's bin refined into NBINS sub-bins
+    unsigned int *fine[2];     // exact selection: every bin's NBINS sub-bins (+1 spare), by parity
     int exact_select;          // selection_mode "exact" (two-level k-selection) vs "approximate_strided"
     Ctrl *ctrl;
     // config
@@ -270,6 +270,20 @@ __device__ __forceinline__ int key_bin(double key, double base, double w) {
     if (!(f >= 0.0)) return 0;
     if (f >= (double)NBINS) return NBINS;
     return (int)f;
+}
+
+// exact selection (two-barrier solver): the key's sub-bin inside its
+// coarse bin cb, counted as the key is histogrammed -- the bin that holds
+// the K-th key is then refined without a second pass over the keys and a
+// second grid barrier.  Same lo / sub-width arithmetic as a refinement
+// pass over that bin.
+constexpr size_t FINE_ROW = NBINS + 1;
+constexpr size_t FINE_N = (size_t)NBINS * FINE_ROW;
+__device__ __forceinline__ void fine_add(unsigned int *fine, double key, double base, double w, int cb) {
+    if (cb >= NBINS) return;
+    const double lo = base + (double)cb * w, sw = w / (double)NBINS;
+    const double f = (key - lo) / sw;
+    if (f >= 0.0 && f < (double)NBINS) atomicAdd(fine + (size_t)cb * FINE_ROW + (int)f, 1u);
 }
 
 __device__ __forceinline__ void store_win(const WinSoA &W, unsigned long long i, const Win &c) {
@@ -1110,11 +1124,13 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         if (blockIdx.x == 0) {
             if (threadIdx.x < sizeof(Slot) / 8)
                 reinterpret_cast<unsigned long long *>(&nxt)[threadIdx.x] = 0ull;
-            for (int b = threadIdx.x; b <= NBINS; b += TPB) {
-                p.hist[(it + 1) & 1][b] = 0u;
-                p.hist2[(it + 1) & 1][b] = 0u;
-            }
+            for (int b = threadIdx.x; b <= NBINS; b += TPB) p.hist[(it + 1) & 1][b] = 0u;
             if (threadIdx.x == 0) ls.max(ST_PEAK, nS + nP);
+        }
+        if (p.exact_select) {
+            // the next iteration's sub-bins (last read in phase B of it-1)
+            uint4 *fz = reinterpret_cast<uint4 *>(p.fine[(it + 1) & 1]);
+            for (unsigned long long q = gtid; q < FINE_N / 4; q += gthreads) fz[q] = make_uint4(0u, 0u, 0u, 0u);
         }
         unsigned int *hcur = p.hist[it & 1];
         // write one window into pool slot nP + rel (children C_i follow P_i)
@@ -1122,7 +1138,9 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             unsigned long long slot = nP + rel;
             if ((long long)slot < p.cap) {
                 store_win(X, slot, c);
-                atomicAdd(s_hist + key_bin(c.key, base, w), 1u);
+                const int cb = key_bin(c.key, base, w);
+                atomicAdd(s_hist + cb, 1u);
+                if (p.exact_select) fine_add(p.fine[it & 1], c.key, base, w, cb);
             } else {
                 atomicExch(&ctrl->error, ERR_OVERFLOW);
             }
@@ -1230,23 +1248,13 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         // ================= phase B: organise =================
         Thresh th = pick_threshold(hcur, base, w, p.K);
         if (p.exact_select && th.bin < NBINS) {
-            // selection_mode "exact" (engine.py:256, argpartition): refine
-            // the bin holding the K-th key into NBINS sub-bins (one more
-            // pass over the keys and one more grid barrier), so the batch is
-            // the K nearest windows up to keys within (bin width / NBINS)
+            // selection_mode "exact" (engine.py:256, argpartition): the bin
+            // holding the K-th key refined into its NBINS sub-bins (counted
+            // with the keys, fine_add), so the batch is the K nearest
+            // windows up to keys within (bin width / NBINS)
             const double lo = base + (double)th.bin * w, sw = w / (double)NBINS;
-            const unsigned long long nC2 = *(volatile unsigned long long *)&cur.nC;
-            unsigned long long tot2 = nP + nC2;
-            if ((long long)tot2 > p.cap) tot2 = p.cap;
-            for (unsigned long long i = gtid; i < tot2; i += gthreads) {
-                const double k = __ldcg(X.key + i);
-                const double f = (k - lo) / sw;
-                if (f >= 0.0 && f < (double)NBINS) atomicAdd(s_hist + (int)f, 1u);
-            }
-            unsigned int *h2 = p.hist2[it & 1];
-            flush_hist(s_hist, h2);
-            grid_barrier(ctrl, gen);
-            const Thresh t2 = pick_threshold(h2, lo, sw, (long long)((unsigned long long)p.K - th.before));
+            const Thresh t2 = pick_threshold(p.fine[it & 1] + (size_t)th.bin * FINE_ROW, lo, sw,
+                                             (long long)((unsigned long long)p.K - th.before));
             if (t2.bin < NBINS) th.t = t2.t;
         }
         phase(ST_PH_SELECT);
@@ -1302,7 +1310,9 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 if (sel) store_win(p.S, s_sb[0] + (ex & 0xffffu), c);
                 if (keep) {
                     store_win(Y, s_sb[1] + (ex >> 16), c);
-                    atomicAdd(s_hist + key_bin(c.key, nbase, th.w_next), 1u);
+                    const int cb = key_bin(c.key, nbase, th.w_next);
+                    atomicAdd(s_hist + cb, 1u);
+                    if (p.exact_select) fine_add(p.fine[(it + 1) & 1], c.key, nbase, th.w_next, cb);
                 }
                 __syncthreads();
                 if (p.prof && valid) {
@@ -1904,7 +1914,6 @@ __global__ void k_init_state(Params p, const int64_t *src, int nsrc) {
     for (long long j = t0; j < nher; j += n) p.split_new[j] = make_ulonglong2(ord64(INFINITY), ord64(0.0));
     for (long long b = t0; b < 2 * (NBINS + 1); b += n) {
         (b <= NBINS ? p.hist[0][b] : p.hist[1][b - NBINS - 1]) = 0u;
-        (b <= NBINS ? p.hist2[0][b] : p.hist2[1][b - NBINS - 1]) = 0u;
     }
     if (t0 == 0)
         for (int q = 0; q < NSLOT; ++q) p.ctrl->slot[q].pmin = ~0ull;
@@ -2134,8 +2143,8 @@ static int ensure_ws(pch_mesh *m, long long cap, int rows, bool exact = false) {
     if ((rc = alloc_soa4(m, p, cap))) return rc;
     if ((rc = ws_alloc(m, &p.hist[0], NBINS + 1))) return rc;
     if ((rc = ws_alloc(m, &p.hist[1], NBINS + 1))) return rc;
-    if ((rc = ws_alloc(m, &p.hist2[0], NBINS + 1))) return rc;
-    if ((rc = ws_alloc(m, &p.hist2[1], NBINS + 1))) return rc;
+    if ((rc = ws_alloc(m, &p.fine[0], 2 * FINE_N))) return rc;
+    p.fine[1] = p.fine[0] + FINE_N;
     if ((rc = ws_alloc(m, &p.ctrl, 1))) return rc;
     if ((rc = ws_alloc(m, &p.ccnt, 2 * 3 * MAX_CTAS))) return rc;
     p.cap = cap;
@@ -2311,6 +2320,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         CK(cudaMemsetAsync(p.ctrl, 0, sizeof(Ctrl), st));
         p.live_grid = m->grid_live;
         if (p.live) CK(cudaMemsetAsync(p.ccnt, 0, sizeof(unsigned int) * 2 * 3 * MAX_CTAS, st));
+        if (!p.live && p.exact_select) CK(cudaMemsetAsync(p.fine[0], 0, sizeof(unsigned int) * 2 * FINE_N, st));
         k_init_state<<<4 * 148, 256, 0, st>>>(p, d_src, nsrc);
         CK(cudaGetLastError());
         k_set_sources<<<(nsrc + 255) / 256, 256, 0, st>>>(p, d_src, nsrc);

@@ -1246,6 +1246,22 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             p.trace[(size_t)it * TR_N + TR_B1] = globaltimer();
 
         // ================= phase B: organise =================
+        // the shadow-table commit needs no threshold: its first entries and
+        // their new values are read here, in flight during the threshold
+        // pick, and written after it
+        const unsigned long long nTVc = [&] {
+            const unsigned long long n = *(volatile unsigned long long *)&cur.nTV;
+            return n < (unsigned long long)p.tvcap ? n : (unsigned long long)p.tvcap;
+        }();
+        const unsigned long long nTEc = [&] {
+            const unsigned long long n = *(volatile unsigned long long *)&cur.nTE;
+            return n < (unsigned long long)p.tecap ? n : (unsigned long long)p.tecap;
+        }();
+        const int32_t cv = gtid < nTVc ? __ldcg(p.tv_list + gtid) : -1;
+        const int32_t cj = gtid < nTEc ? __ldcg(p.te_list + gtid) : -1;
+        const unsigned long long cdist = cv >= 0 ? __ldcg(p.dist_new + cv) : 0ull;
+        const ulonglong2 csplit = cj >= 0 ? __ldcg(p.split_new + cj) : make_ulonglong2(0ull, 0ull);
+        const int32_t cfv = gtid < nFc ? fe[gtid].v : -1;  // fan picks consumed in A: reset below
         Thresh th = pick_threshold(hcur, base, w, p.K);
         if (p.exact_select && th.bin < NBINS) {
             // selection_mode "exact" (engine.py:256, argpartition): the bin
@@ -1260,27 +1276,21 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         phase(ST_PH_SELECT);
         {
             // commit the shadow tables for entries touched this iteration
-            const unsigned long long nTV = *(volatile unsigned long long *)&cur.nTV;
-            const unsigned long long nTVc = nTV < (unsigned long long)p.tvcap ? nTV : p.tvcap;
-            for (unsigned long long i = gtid; i < nTVc; i += gthreads) {
+            if (cv >= 0) p.dist_cur[cv] = __longlong_as_double((long long)cdist);
+            if (cj >= 0) p.split_cur[cj] = make_double2(unord64(csplit.x), unord64(csplit.y));
+            for (unsigned long long i = gtid + gthreads; i < nTVc; i += gthreads) {
                 int32_t v = __ldcg(p.tv_list + i);
                 p.dist_cur[v] = __longlong_as_double((long long)__ldcg(p.dist_new + v));
             }
-            const unsigned long long nTE = *(volatile unsigned long long *)&cur.nTE;
-            const unsigned long long nTEc = nTE < (unsigned long long)p.tecap ? nTE : p.tecap;
-            for (unsigned long long i = gtid; i < nTEc; i += gthreads) {
+            for (unsigned long long i = gtid + gthreads; i < nTEc; i += gthreads) {
                 int32_t j = __ldcg(p.te_list + i);
                 ulonglong2 s = __ldcg(p.split_new + j);
                 p.split_cur[j] = make_double2(unord64(s.x), unord64(s.y));
             }
             // fan picks of iteration it-1 are consumed: reset them
-            if (it > 0) {
-                const unsigned long long nF = *(volatile unsigned long long *)&prev.nF;
-                const FanEv *fe = p.fanev[(it + 2) % 3];
-                const unsigned long long nFc = nF < (unsigned long long)p.fancap ? nF : p.fancap;
-                for (unsigned long long i = gtid; i < nFc; i += gthreads)
-                    p.fanpick[(it + 2) % 3][fe[i].v] = make_ulonglong2(~0ull, ~0ull);
-            }
+            if (cfv >= 0) p.fanpick[(it + 2) % 3][cfv] = make_ulonglong2(~0ull, ~0ull);
+            for (unsigned long long i = gtid + gthreads; i < nFc; i += gthreads)
+                p.fanpick[(it + 2) % 3][fe[i].v] = make_ulonglong2(~0ull, ~0ull);
         }
         phase(ST_PH_EVENTS);
         {

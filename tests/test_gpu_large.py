@@ -183,8 +183,8 @@ def test_config_knot4m_exact(case):
     """configs[2], the 4M-face torus knot, in the configuration exact on it
     (two-barrier solver, 1e-4 rad fan margin; 27 s): the
     strict rule against the reference's full-fan oracle where the fixture
-    holds it (knot4m: 2.4 h of oracle CPU time; measured max relative error
-    1.2e-14, every vertex reached); otherwise every vertex reached, never
+    holds it (2.4 h of oracle CPU time each; measured max relative error
+    1.2e-14 / 1.3e-14, every vertex reached); otherwise every vertex reached, never
     longer than the reference's default mode on any sampled vertex, shorter
     only on the few it detoured, edge-Lipschitz everywhere."""
     from paper_1305_1293_b200 import EngineConfig, run_pch

@@ -1436,6 +1436,16 @@ __device__ __forceinline__ void warp_chunk_alloc2(unsigned long long *s_cnt, uns
 // PHASE: attribute warp cycles to the four phases (RunStats.time_*), on
 // request only (EngineConfig.phase_times): the clock reads and per-item
 // shared adds on the batch warps' critical path cost ~3 % of a field
+// development instrumentation (PCH_TRACE timelines, PCH_PROFILE clocks) of
+// the one-barrier solver: compiled in only with -DPCH_DEVTOOLS, so the
+// default kernel carries no checks for it
+#ifdef PCH_DEVTOOLS
+#define DEV_TRACE (p.trace != nullptr)
+#define DEV_PROF (p.prof != 0)
+#else
+#define DEV_TRACE false
+#define DEV_PROF false
+#endif
 template <bool PHASE>
 __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     // Outputs are chunked per CTA: CTA b writes the windows it routes to
@@ -1581,8 +1591,8 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             clr.smax = 0ull;
             ls.max(ST_PEAK, (unsigned long long)nS + nP);
         }
-        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_START_MAX);
-        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (DEV_TRACE && threadIdx.x == 0) trace_max(p, it, TR_START_MAX);
+        if (DEV_TRACE && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *tr = p.trace + (size_t)it * TR_N;
             tr[TR_T0] = globaltimer();
             tr[TR_NS] = nS;
@@ -1640,19 +1650,19 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             if (wi < nwS) {
                 const unsigned int i = (wi << 5) + lane;
                 if (i < nS) {
-                    long long c0 = p.prof ? clock64() : 0;
+                    long long c0 = DEV_PROF ? clock64() : 0;
                     const unsigned long long slot0 = chunk_slot(s_pre[0], G, i, ch);
-                    if (p.trace) {
+                    if (DEV_TRACE) {
                         asm volatile("" ::"l"(slot0));
                         trace_max_warp(p, it, TR_TRIP0);
                     }
                     Win win = load_win(p.S, (unsigned long long)rSc * (unsigned long long)p.cap + slot0);
-                    if (p.trace) {
+                    if (DEV_TRACE) {
                         asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
                         trace_max_warp(p, it, TR_LOADED);
                     }
                     long long c1 = 0;
-                    if (p.prof) {
+                    if (DEV_PROF) {
                         asm volatile("" ::"d"(win.b0 + win.b1 + win.d0 + win.d1 + win.d + (double)win.jo));
                         c1 = clock64();
                     }
@@ -1679,11 +1689,11 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                         win = take1 ? o1 : o0;
                         no = 0;
                     }
-                    if (p.trace) {
+                    if (DEV_TRACE) {
                         asm volatile("" ::"d"((no > 0 ? o0.key : 0.0) + (no > 1 ? o1.key : 0.0)));
                         trace_max_warp(p, it, TR_WORK_END);
                     }
-                    if (p.prof) {
+                    if (DEV_PROF) {
                         asm volatile("" ::"d"((no > 0 ? o0.key : 0.0) + (no > 1 ? o1.key : 0.0)));
                         const long long c2p = clock64();
                         ls.add(ST_CYC_PROP, c2p - c0);
@@ -1776,8 +1786,8 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             if (no > 1) put_at(s1, s1 ? sa++ : pa++, o1);
             if (h2) put_at(s2, s2 ? sa : pa, o2);
             ls.add(ST_STORED, (unsigned long long)(no + (h2 ? 1 : 0)));
-            if (p.trace && wi < nwS) trace_max_warp(p, it, TR_ROUTED);
-            if (p.trace && wi < nwS) trace_max_warp(p, it, TR_SCAN_END);
+            if (DEV_TRACE && wi < nwS) trace_max_warp(p, it, TR_ROUTED);
+            if (DEV_TRACE && wi < nwS) trace_max_warp(p, it, TR_SCAN_END);
             if (PHASE && lane == 0) {
                 const long long now = clock64();
                 atomicAdd(&s_st[ST_PH_COMPACT], (unsigned long long)(now - ph_t));
@@ -1829,7 +1839,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 s_pmin = ~0ull;
                 s_smax = 0ull;
             }
-            if (p.trace) trace_max(p, it, TR_A_END);
+            if (DEV_TRACE) trace_max(p, it, TR_A_END);
             if (blockIdx.x == 0) {
                 if (p.max_iter >= 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
                 if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
@@ -1869,7 +1879,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         build_prefix(par ^ 1, par, &nxt);
         const int err = (int)s_c[0];
         const unsigned int ns = s_pre[0][G], np = s_pre[1][G], nf = s_pre[2][G];
-        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (DEV_TRACE && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *trr = p.trace + (size_t)it * TR_N;
             trr[TR_B1] = trr[TR_B_END] = trr[TR_B2] = globaltimer();
             trr[TR_NC] = (unsigned long long)ns + np;

@@ -7,7 +7,8 @@ controller step floor / fixed step, in mean edge lengths.)
 
 Each configuration is run 3 times (best device time reported) and checked
 against the sequential ICH oracle (test infrastructure, checker only).
-With --trace, PCH_TRACE is set and the per-iteration timeline of the last
+With --trace (needs a -DPCH_DEVTOOLS build, PCH_B200_LIB=altlib/dev/...),
+PCH_TRACE is set and the per-iteration timeline of the last
 run is summarised (phase A / barrier / phase B shares).
 """
 import os

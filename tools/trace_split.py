@@ -1,7 +1,10 @@
 """Per-iteration timeline of one traced solve, split into iterations that
 end with a grid barrier and CTA-local ones (development tool).
 
-    python tools/trace_split.py WORKLOAD
+    PCH_B200_LIB=altlib/dev/libpch_b200.so python tools/trace_split.py WORKLOAD
+
+(the library built with tools/build_variant.sh dev -DPCH_DEVTOOLS: the
+default build carries no trace instrumentation)
 """
 import os
 import sys

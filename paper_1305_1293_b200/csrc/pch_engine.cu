@@ -418,6 +418,17 @@ constexpr int FE_CAP = 2 * TPB;
 
 
 
+// development instrumentation (PCH_TRACE timelines, PCH_PROFILE clocks) of
+// the solvers: compiled in only with -DPCH_DEVTOOLS, so the
+// default kernels carry no checks for it
+#ifdef PCH_DEVTOOLS
+#define DEV_TRACE (p.trace != nullptr)
+#define DEV_PROF (p.prof != 0)
+#else
+#define DEV_TRACE false
+#define DEV_PROF false
+#endif
+
 struct Stage {
     unsigned int ntv, nte, nfe, pad;
     int32_t tv[3 * TPB];  // improved vertices (<= 3 per propagation)
@@ -455,7 +466,7 @@ __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, S
     }
     int tries = 0;
     const bool won = cas_min_u128(t.split + j, ord64(comp), ord64(entry), guess, &tries);
-    if (p.prof) {
+    if (DEV_PROF) {
         atomicAdd(&p.ctrl->st[ST_CAS_ANGLE_CALLS], 1ull);
         atomicAdd(&p.ctrl->st[ST_CAS_ANGLE_TRIES], (unsigned long long)tries);
     }
@@ -500,7 +511,7 @@ __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uin
     } else {
         int tries = 0;
         cas_min_u128(t.pick + v, hi, lo, guess, &tries);
-        if (p.prof) {
+        if (DEV_PROF) {
             atomicAdd(&p.ctrl->st[ST_CAS_FAN_CALLS], 1ull);
             atomicAdd(&p.ctrl->st[ST_CAS_FAN_TRIES], (unsigned long long)tries);
         }
@@ -1105,7 +1116,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         Slot &nxt = ctrl->slot[(it + 1) % 3];
         const unsigned long long nS = *(volatile unsigned long long *)&cur.nS;
         const unsigned long long nP = *(volatile unsigned long long *)&cur.nP;
-        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (DEV_TRACE && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *tr = p.trace + (size_t)it * TR_N;
             tr[TR_T0] = globaltimer();
             tr[TR_NS] = nS;
@@ -1159,7 +1170,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         }();
         const FanEv *fe = p.fanev[(it + 2) % 3];
         auto fan_event_warp = [&](unsigned long long i, Win &c, unsigned int &n) {
-            long long c3 = p.prof ? clock64() : 0;
+            long long c3 = DEV_PROF ? clock64() : 0;
             FanEv e = fe[i];
             const double rel = fan_rel(e);
             const double dv = __ldcg(p.dist_cur + e.v);
@@ -1183,7 +1194,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                              [&](const Win &x) { put_pool(x, warp_alloc(&cur.nC, true)); }, ls,
                              p.dup_epoch + it + 1u);
             }
-            if (p.prof) {
+            if (DEV_PROF) {
                 ls.add(ST_CYC_FANITEM, clock64() - c3);
                 ls.add(ST_N_FANITEM);
             }
@@ -1203,22 +1214,22 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 Win ca, cb;
                 int nc = 0;
                 if (i < nS) {
-                    long long c0 = p.prof ? clock64() : 0;
+                    long long c0 = DEV_PROF ? clock64() : 0;
                     Win win = load_win(p.S, i);
                     nc = propagate(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, win, ca,
                                    cb, ls);
-                    if (p.prof) ls.add(ST_CYC_PROP, clock64() - c0);
+                    if (DEV_PROF) ls.add(ST_CYC_PROP, clock64() - c0);
                     if (nc > maxchild) maxchild = nc;
                 } else if (t + 1 == trips && gwid >= busyw && gwid - busyw < nFa) {
                     unsigned int n = 0;
                     fan_event_warp(gwid - busyw, ca, n);
                     nc = (int)n;
                 }
-                long long c2 = p.prof ? clock64() : 0;
+                long long c2 = DEV_PROF ? clock64() : 0;
                 const unsigned long long rel = trip_flush(p, sg, cur, it, (unsigned int)nc);
                 if (nc > 0) put_pool(ca, rel);
                 if (nc > 1) put_pool(cb, rel + 1);
-                if (p.prof) {
+                if (DEV_PROF) {
                     ls.add(ST_CYC_POOL, clock64() - c2);
                     ls.add(ST_N_POOL);
                 }
@@ -1239,10 +1250,10 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             }
         }
         flush_hist(s_hist, hcur);
-        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_A_END);
+        if (DEV_TRACE && threadIdx.x == 0) trace_max(p, it, TR_A_END);
         phase(ST_PH_EVENTS);
         grid_barrier(ctrl, gen);
-        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0)
+        if (DEV_TRACE && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0)
             p.trace[(size_t)it * TR_N + TR_B1] = globaltimer();
 
         // ================= phase B: organise =================
@@ -1304,7 +1315,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             __shared__ unsigned long long s_sb[2];
             for (unsigned long long t = 0; t < trips; ++t) {
                 const unsigned long long i = t * gthreads + gtid;
-                long long c5 = p.prof ? clock64() : 0;
+                long long c5 = DEV_PROF ? clock64() : 0;
                 Win c;
                 const bool valid = i < total;
                 if (valid) c = load_win(X, i);
@@ -1325,7 +1336,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                     if (p.exact_select) fine_add(p.fine[(it + 1) & 1], c.key, nbase, th.w_next, cb);
                 }
                 __syncthreads();
-                if (p.prof && valid) {
+                if (DEV_PROF && valid) {
                     ls.add(ST_CYC_PART, clock64() - c5);
                     ls.add(ST_N_PART);
                 }
@@ -1336,7 +1347,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
             if (p.max_iter >= 0 && it + 1 > p.max_iter) atomicExch(&ctrl->error, ERR_GUARD);
             if (globaltimer() - t_start > p.time_limit_ns) atomicExch(&ctrl->error, ERR_TIMEOUT);
         }
-        if (p.trace && threadIdx.x == 0) trace_max(p, it, TR_B_END);
+        if (DEV_TRACE && threadIdx.x == 0) trace_max(p, it, TR_B_END);
         grid_barrier(ctrl, gen);
         phase(ST_PH_COMPACT);
 
@@ -1345,7 +1356,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
         const unsigned long long ns = *(volatile unsigned long long *)&nxt.nS;
         const unsigned long long np = *(volatile unsigned long long *)&nxt.nP;
         const unsigned long long nf = *(volatile unsigned long long *)&cur.nF;
-        if (p.trace && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
+        if (DEV_TRACE && it < p.trace_cap && blockIdx.x == 0 && threadIdx.x == 0) {
             unsigned long long *tr = p.trace + (size_t)it * TR_N;
             tr[TR_B2] = globaltimer();
             tr[TR_NC] = *(volatile unsigned long long *)&cur.nC;
@@ -1436,16 +1447,6 @@ __device__ __forceinline__ void warp_chunk_alloc2(unsigned long long *s_cnt, uns
 // PHASE: attribute warp cycles to the four phases (RunStats.time_*), on
 // request only (EngineConfig.phase_times): the clock reads and per-item
 // shared adds on the batch warps' critical path cost ~3 % of a field
-// development instrumentation (PCH_TRACE timelines, PCH_PROFILE clocks) of
-// the one-barrier solver: compiled in only with -DPCH_DEVTOOLS, so the
-// default kernel carries no checks for it
-#ifdef PCH_DEVTOOLS
-#define DEV_TRACE (p.trace != nullptr)
-#define DEV_PROF (p.prof != 0)
-#else
-#define DEV_TRACE false
-#define DEV_PROF false
-#endif
 template <bool PHASE>
 __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     // Outputs are chunked per CTA: CTA b writes the windows it routes to

@@ -229,11 +229,15 @@ struct RowTabs {
     ulonglong2 *pick;          // fan picks
 };
 
+// LIVE: 1 / 0 when the caller is the one- / two-barrier solver (the
+// other solver's branches then compile away), -1 to read p.live
+template <int LIVE = -1>
 __device__ __forceinline__ RowTabs row_tabs(const Params &p, uint32_t r, int it) {
+    const bool live = LIVE < 0 ? (p.live != 0) : (LIVE != 0);
     RowTabs t;
     t.dist = p.dist_new + (size_t)r * p.nv;
     t.split = p.split_new + (size_t)r * p.nhe;
-    t.pick = p.fanpick[p.live ? 0 : it % 3] + (size_t)r * p.nv;
+    t.pick = p.fanpick[live ? 0 : it % 3] + (size_t)r * p.nv;
     return t;
 }
 
@@ -241,15 +245,19 @@ __device__ __forceinline__ RowTabs row_tabs(const Params &p, uint32_t r, int it)
 // (deterministic solver, one row), or the shadow tables the events update
 // atomically.  Any value read is the length of a real path, so a stale or
 // racing read only weakens pruning; it never admits a wrong distance.
+template <int LIVE = -1>
 __device__ __forceinline__ double gdist(const Params &p, const RowTabs &t, int32_t v) {
-    if (p.live) return __longlong_as_double((long long)__ldcg(t.dist + v));
+    const bool live = LIVE < 0 ? (p.live != 0) : (LIVE != 0);
+    if (live) return __longlong_as_double((long long)__ldcg(t.dist + v));
     return __ldcg(p.dist_cur + v);
 }
 // the angle-split entry as ord64 bits (the CAS guess), converted where it
 // is used: keeping the conversion away from the load lets the load's
 // latency overlap the unfolding and both children's geometry
+template <int LIVE = -1>
 __device__ __forceinline__ ulonglong2 gsplit_raw(const Params &p, const RowTabs &t, int32_t j) {
-    if (p.live) {
+    const bool live = LIVE < 0 ? (p.live != 0) : (LIVE != 0);
+    if (live) {
         // single-copy-atomic 128-bit read (a strong .b128 load): the pair is
         // never torn between two claims' CAS writes
         unsigned long long lo, hi;
@@ -436,23 +444,27 @@ struct Stage {
     FanEv fe[FE_CAP];     // saddle fan candidates (overflow appends directly)
 };
 
+template <int LIVE = -1>
 __device__ __forceinline__ void dist_event(const Params &p, const RowTabs &t, Stage &sg, int32_t v,
                                            double cand, LocalStats &ls) {
+    const bool live = LIVE < 0 ? (p.live != 0) : (LIVE != 0);
     // the caller checked cand against the distance it read; the minimum
     // itself needs no reply (RED), the vertex is listed for the commit
     ls.add(ST_EV_CREATED);
     atomicMin(t.dist + v, (unsigned long long)__double_as_longlong(cand));
-    if (!p.live) {
+    if (!live) {
         unsigned int k = atomicAdd(&sg.ntv, 1u);
         sg.tv[k] = v;
     }
     ls.add(ST_EV_APPLIED);
 }
 
+template <int LIVE = -1>
 __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, Stage &sg, int32_t j,
                                             double comp, double entry, ulonglong2 guess, LocalStats &ls) {
+    const bool live = LIVE < 0 ? (p.live != 0) : (LIVE != 0);
     ls.add(ST_EV_CREATED);
-    if (p.live) {
+    if (live) {
         // live solver: one CAS attempt, reply unused (off the propagation's
         // critical path).  A lost race leaves the entry at a value that is
         // still smaller than the one read -- a window that kept both its
@@ -471,7 +483,7 @@ __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, S
         atomicAdd(&p.ctrl->st[ST_CAS_ANGLE_TRIES], (unsigned long long)tries);
     }
     if (won) {
-        if (!p.live) {
+        if (!live) {
             unsigned int k = atomicAdd(&sg.nte, 1u);
             sg.te[k] = j;
         }
@@ -479,10 +491,11 @@ __device__ __forceinline__ void angle_event(const Params &p, const RowTabs &t, S
     }
 }
 
-template <typename FanSink>
+template <int LIVE = -1, typename FanSink>
 __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uint32_t row, FanSink &&sink,
                                           ulonglong2 guess, int32_t v, int32_t anchor,
                                           double cand, double ax, double ay, double bx, double by) {
+    const bool live = LIVE < 0 ? (p.live != 0) : (LIVE != 0);
     FanEv e;
     e.v = v;
     e.row = row;
@@ -502,7 +515,7 @@ __device__ __forceinline__ void fan_event(const Params &p, const RowTabs &t, uin
     // CAS with the pick it read.
     const unsigned long long hi = (unsigned long long)__double_as_longlong(cand);
     const unsigned long long lo = fan_tiebreak(e);
-    if (p.live) {
+    if (live) {
         // one attempt, reply unused (no wait on the propagation path): if
         // it loses a race against a worse candidate, the winner check of
         // the next iteration finds the pick stale and repairs it
@@ -781,9 +794,10 @@ __device__ void emit_fan(const Params &p, const RowTabs &t, uint32_t row, int32_
 // Algorithm 2 (geom.py:312) for one window against the frozen tables.
 // Up to two children are returned in `c`; events go to the shadow tables.
 
-template <typename FanSink>
+template <int LIVE = -1, typename FanSink>
 __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, FanSink &&fsink,
                                          const Win &w, Win &out0, Win &out1, LocalStats &ls) {
+    const bool live = LIVE < 0 ? (p.live != 0) : (LIVE != 0);
     // Latency layout: the per-iteration critical path is one propagation
     // (of the slowest lane of the slowest warp), so
     //  * every memory access is issued as soon as its address is known
@@ -797,7 +811,7 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const int32_t j = w.he, jo = w.jo;
     const double b0 = w.b0, b1 = w.b1, d0 = w.d0, d1 = w.d1, dps = w.d;
     const bool far = jo >= 0;
-    const RowTabs T = row_tabs(p, w.row, it);
+    const RowTabs T = row_tabs<LIVE>(p, w.row, it);
     // level 1: the far face (or, on a boundary, the window's own face)
     // and the angle-split entry of j
     const int32_t fr = far ? jo : j;
@@ -817,18 +831,18 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     const uint32_t v0f = w.v0f, v1f = w.v1f, vdf = far ? w.vdf : 0u;
     const int32_t cho_l = __ldg(&fp->opp[a1]), cho_r = __ldg(&fp->opp[a2]);
     const uint32_t apx_l = __ldg(&fp->apx[a1]), apx_r = __ldg(&fp->apx[a2]);
-    const ulonglong2 sp_raw = far ? gsplit_raw(p, T, j) : make_ulonglong2(ord64(INFINITY), ord64(0.0));
+    const ulonglong2 sp_raw = far ? gsplit_raw<LIVE>(p, T, j) : make_ulonglong2(ord64(INFINITY), ord64(0.0));
     // level 2: distances at the three vertices
     const int32_t v0 = (int32_t)(v0f & VMASK), v1 = (int32_t)(v1f & VMASK);
     const int32_t vd = (int32_t)(vdf & VMASK);
-    const double g0 = gdist(p, T, v0), g1 = gdist(p, T, v1);
-    const double gdd = far ? gdist(p, T, vd) : INFINITY;
+    const double g0 = gdist<LIVE>(p, T, v0), g1 = gdist<LIVE>(p, T, v1);
+    const double gdd = far ? gdist<LIVE>(p, T, vd) : INFINITY;
     // saddle endpoints: the current fan pick, the guess for its CAS-min
     const ulonglong2 *pick = T.pick;
     const ulonglong2 none = make_ulonglong2(~0ull, ~0ull);
-    const ulonglong2 pk0 = (p.live && (v0f & SADDLE_BIT)) ? __ldcg(pick + v0) : none;
-    const ulonglong2 pk1 = (p.live && (v1f & SADDLE_BIT)) ? __ldcg(pick + v1) : none;
-    const ulonglong2 pkd = (p.live && far && (vdf & SADDLE_BIT)) ? __ldcg(pick + vd) : none;
+    const ulonglong2 pk0 = (live && (v0f & SADDLE_BIT)) ? __ldcg(pick + v0) : none;
+    const ulonglong2 pk1 = (live && (v1f & SADDLE_BIT)) ? __ldcg(pick + v1) : none;
+    const ulonglong2 pkd = (live && far && (vdf & SADDLE_BIT)) ? __ldcg(pick + vd) : none;
 
     double ix, iy;
     if (!unfold(b0, b1, d0, d1, ix, iy)) {
@@ -918,19 +932,19 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
     nc = (sl ? 1 : 0) + (sr ? 1 : 0);
 
     // ---- events, issued together (order independent: min / CAS-min) ----
-    if (ev0) dist_event(p, T, sg, v0, cand0, ls);
-    if (ev1) dist_event(p, T, sg, v1, cand1, ls);
-    if (evd) dist_event(p, T, sg, vd, candd, ls);
-    if (claim) angle_event(p, T, sg, j, comp, entry_x, sp_raw, ls);
+    if (ev0) dist_event<LIVE>(p, T, sg, v0, cand0, ls);
+    if (ev1) dist_event<LIVE>(p, T, sg, v1, cand1, ls);
+    if (evd) dist_event<LIVE>(p, T, sg, vd, candd, ls);
+    if (claim) angle_event<LIVE>(p, T, sg, j, comp, entry_x, sp_raw, ls);
     // saddle fans (Fig. 3c): the reverse direction of the incoming ray
     // relative to an anchor half-edge out of the vertex (geom.py:353-484)
-    if (ev0 && (v0f & SADDLE_BIT)) fan_event(p, T, w.row, fsink, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
+    if (ev0 && (v0f & SADDLE_BIT)) fan_event<LIVE>(p, T, w.row, fsink, pk0, v0, j, cand0, ix, iy, 1.0, 0.0);
     if (ev1 && (v1f & SADDLE_BIT)) {
         if (far) {
             // anchor jo = v1 -> v0: its wedge follows next(j)'s, so this is
             // the reference's anchor next(j) with the corner at v1 folded
             // into the anchor angle
-            fan_event(p, T, w.row, fsink, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
+            fan_event<LIVE>(p, T, w.row, fsink, pk1, v1, jo, cand1, ix - ell, iy, -1.0, 0.0);
         } else {
             // boundary window: anchor next(j), the source-side apex
             // direction from v1 (geom.py:372-377)
@@ -941,12 +955,12 @@ __device__ __forceinline__ int propagate(const Params &p, Stage &sg, int it, Fan
             const double lps = __ldg(&fj->len[b == 0 ? 2 : b - 1]);
             const double axs = 0.5 * (ell * ell + lps * lps - lns * lns) / ell;
             const double ay2 = lps * lps - axs * axs;
-            fan_event(p, T, w.row, fsink, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
+            fan_event<LIVE>(p, T, w.row, fsink, pk1, v1, jn, cand1, ix - ell, iy, axs - ell,
                       ay2 > 0.0 ? sqrt(ay2) : 0.0);
         }
     }
     if (evd && (vdf & SADDLE_BIT))
-        fan_event(p, T, w.row, fsink, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
+        fan_event<LIVE>(p, T, w.row, fsink, pkd, vd, 3 * (jo / 3) + a2, candd, ix - dx, iy - dy, ell - dx, -dy);
     return nc;
 }
 
@@ -1216,7 +1230,7 @@ __global__ void __launch_bounds__(TPB, PCH_MIN_BLOCKS) pch_persistent(Params p) 
                 if (i < nS) {
                     long long c0 = DEV_PROF ? clock64() : 0;
                     Win win = load_win(p.S, i);
-                    nc = propagate(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, win, ca,
+                    nc = propagate<0>(p, sg, it, StageFanSink{p, sg, &cur.nF, p.fanev[it % 3]}, win, ca,
                                    cb, ls);
                     if (DEV_PROF) ls.add(ST_CYC_PROP, clock64() - c0);
                     if (nc > maxchild) maxchild = nc;
@@ -1671,7 +1685,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                     // (key <= t_{i+1}) is propagated right away by the same
                     // thread, up to p.chain propagations
                     for (int step = 1;; ++step) {
-                        no = propagate(p, sg, it, fsink, win, o0, o1, ls);
+                        no = propagate<1>(p, sg, it, fsink, win, o0, o1, ls);
                         if (no > maxchild) maxchild = no;
                         if (step >= p.chain || no == 0) break;
                         const bool c0ok = o0.key <= tn, c1ok = no > 1 && o1.key <= tn;
@@ -1708,7 +1722,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 const int sl = lane % FAN_LANES;
                 if (fi < nF) {
                     const FanEv e = fev[chunk_slot(s_pre[2], G, fi, chF)];
-                    const RowTabs T = row_tabs(p, e.row, it);
+                    const RowTabs T = row_tabs<1>(p, e.row, it);
                     const unsigned long long dv = __ldcg(T.dist + e.v);
                     const ulonglong2 pk = __ldcg(T.pick + e.v);
                     const double rel = fan_rel(e);

@@ -1570,7 +1570,11 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     int local_left = 0;  // local iterations still to run in this block
     for (; !init_err;) {
         const int par = it & 1;                     // parity of the iteration's inputs
-        const unsigned int nS = s_pre[0][G], nP = s_pre[1][G], nF = it > 0 ? s_pre[2][G] : 0u;
+        // a local iteration reads this CTA's own counts (s_loc) and maps
+        // item i to slot b * ch + i directly; a global one goes through the
+        // prefix tables
+        const unsigned int nS = local ? s_loc[0] : s_pre[0][G], nP = local ? s_loc[1] : s_pre[1][G];
+        const unsigned int nF = it > 0 ? (local ? s_loc[2] : s_pre[2][G]) : 0u;
         const unsigned long long pminb = s_c[1], smaxb = s_c[2];
         Slot &nxt = ctrl->slot[(it + 1) % NSLOT];
         // work distribution: every warp of the grid over all chunks, or (a
@@ -1666,7 +1670,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 const unsigned int i = (wi << 5) + lane;
                 if (i < nS) {
                     long long c0 = DEV_PROF ? clock64() : 0;
-                    const unsigned long long slot0 = chunk_slot(s_pre[0], G, i, ch);
+                    const unsigned long long slot0 = local ? (unsigned long long)b * ch + i : chunk_slot(s_pre[0], G, i, ch);
                     if (DEV_TRACE) {
                         asm volatile("" ::"l"(slot0));
                         trace_max_warp(p, it, TR_TRIP0);
@@ -1721,7 +1725,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 const unsigned int fi = (wi - nwS) * FANS_PER_WARP + lane / FAN_LANES;
                 const int sl = lane % FAN_LANES;
                 if (fi < nF) {
-                    const FanEv e = fev[chunk_slot(s_pre[2], G, fi, chF)];
+                    const FanEv e = fev[local ? (unsigned long long)b * chF + fi : chunk_slot(s_pre[2], G, fi, chF)];
                     const RowTabs T = row_tabs<1>(p, e.row, it);
                     const unsigned long long dv = __ldcg(T.dist + e.v);
                     const ulonglong2 pk = __ldcg(T.pick + e.v);
@@ -1759,7 +1763,8 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             } else {
                 const unsigned int i = ((wi - nwS - nwF) << 5) + lane;
                 if (i < nP) {
-                    o0 = load_win(p.S, (unsigned long long)rPc * (unsigned long long)p.cap + chunk_slot(s_pre[1], G, i, ch));
+                    o0 = load_win(p.S, (unsigned long long)rPc * (unsigned long long)p.cap +
+                                           (local ? (unsigned long long)b * ch + i : chunk_slot(s_pre[1], G, i, ch)));
                     no = 1;
                 }
             }
@@ -1869,15 +1874,6 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 if (b == 0 && threadIdx.x == 0) s_st[ST_BARRIERS] += 1ull;
             }
             __syncthreads();  // s_loc and this CTA's outputs are visible to its warps
-            // prefix tables with only this CTA's chunk filled: the chunk
-            // lookup then maps item i to slot b * ch + i unchanged
-            for (int c = threadIdx.x; c <= G; c += TPB) {
-                const bool after = c > b;
-                s_pre[0][c] = after ? s_loc[0] : 0u;
-                s_pre[1][c] = after ? s_loc[1] : 0u;
-                s_pre[2][c] = after ? s_loc[2] : 0u;
-            }
-            __syncthreads();
             ++it;
             t = tn;
             local = true;

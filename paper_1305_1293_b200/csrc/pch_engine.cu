@@ -410,7 +410,8 @@ constexpr int LONG_CHAIN_FACES = 1 << 18;  // meshes this large chain one more c
 constexpr unsigned int LIGHT_PER_WARP = 4;  // light work items per warp before batch warps take some
 constexpr int DEFAULT_CHAIN = 2;      // propagations a thread may chain per iteration
 constexpr int ANISO_CHAIN = 6;        // ... on large anisotropic meshes
-constexpr int LOCAL_ITERS = 8;        // live solver: iterations per grid barrier
+constexpr int LOCAL_ITERS = 12;       // live solver: iterations per grid barrier (single fields)
+constexpr int LOCAL_ITERS_ROWS = 8;   // ... batched rows
 constexpr int DEFAULT_ROWS = 32;
 constexpr long long DUP_SLOTS = 1ll << 21;  // fan-window dedupe table (32 MB)
 #ifndef PCH_POOL_MIN
@@ -2264,13 +2265,11 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         p.inv_r02 = p.inv_r0 * p.inv_r0;
         p.fan_widen = cfg->fan_margin;
         // one grid barrier every LOCAL_ITERS iterations, the others CTA-local
-        // (measured: terrain1m 7.64 -> 7.06 ms, sphere16m 112 -> 102 ms;
-        // 16 lets the CTAs' work drift apart: slower).  Single fields on
-        // isotropic meshes only: CTAs running ahead of each other order the
-        // windows more loosely, and on the anisotropic, rounding-sensitive
-        // tori that reopened a few rounding holes per batched row (torus500k,
-        // 10 rows: 0-24 holes, once 1367) for a 1 % gain
-        p.local_iters = LOCAL_ITERS;
+        // (measured: terrain1m 7.64 -> 7.06 ms, sphere16m 112 -> 102 ms at 8;
+        // with local iterations that skip the prefix tables, 12 for single
+        // fields: sphere16m 84.0 -> 81.6 ms, terrain1m / torus500k equal,
+        // 16 lets terrain1m's CTAs drift apart; batched rows stay at 8)
+        p.local_iters = rows > 1 ? LOCAL_ITERS_ROWS : LOCAL_ITERS;
         if (const char *li = getenv("PCH_LOCAL_ITERS")) p.local_iters = std::max(1, atoi(li));  // development
         p.exact_select = cfg->selection_mode == 0 ? 1 : 0;
         // dedupe epochs: solve sequence << 20 plus the iteration (+1), so a

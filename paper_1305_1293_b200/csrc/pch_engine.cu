@@ -1462,7 +1462,7 @@ __device__ __forceinline__ void warp_chunk_alloc2(unsigned long long *s_cnt, uns
 // PHASE: attribute warp cycles to the four phases (RunStats.time_*), on
 // request only (EngineConfig.phase_times): the clock reads and per-item
 // shared adds on the batch warps' critical path cost ~3 % of a field
-template <bool PHASE>
+template <bool PHASE, bool ROWS>
 __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     // Outputs are chunked per CTA: CTA b writes the windows it routes to
     // slots [b*ch, (b+1)*ch) of the next batch / pool and its fan
@@ -1477,20 +1477,24 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     __shared__ unsigned long long s_st[N_ST];
     __shared__ Stage sg;                        // unused staging (shared helpers)
     __shared__ unsigned int s_pre[3][MAX_CTAS + 1];  // prefix tables: S, P, fans(prev)
-    __shared__ unsigned long long s_nsp;        // this CTA's outputs: S (low) / P (high)
-    __shared__ unsigned int s_nf;               // this CTA's fan candidates
+    // this CTA's outputs of iteration i: S (low) / P (high), fan candidates;
+    // three rotating copies, so reading iteration i's totals and clearing
+    // the copy of iteration i+2 need no CTA barrier after the publish one
+    __shared__ unsigned long long s_nsp3[3];
+    __shared__ unsigned int s_nf3[3];
     __shared__ unsigned long long s_pmin, s_smax;
     __shared__ unsigned long long s_c[4];       // err, pmin, smax, grow of the finished iteration
-    __shared__ unsigned int s_loc[3];           // this CTA's own S, P, fan counts (local iterations)
     __shared__ unsigned int s_maxc[3];          // the largest chunk count of each table (build_prefix)
     stats_init(s_st);
     if (threadIdx.x == 0) {
         sg.ntv = sg.nte = sg.nfe = 0u;
         s_pmin = ~0ull;
         s_smax = 0ull;
-        s_nsp = 0ull;
-        s_nf = 0u;
+        s_nsp3[0] = s_nsp3[1] = s_nsp3[2] = 0ull;
+        s_nf3[0] = s_nf3[1] = s_nf3[2] = 0u;
     }
+    int k3 = 0;  // this iteration's copy of the output counters
+    unsigned int locS = 0u, locP = 0u, locF = 0u;  // this CTA's own counts (local iterations)
     LocalStats ls{s_st, false};   // packed per-thread counters, folded when nearly full
     LocalStats lsd{s_st, true};   // rare paths: straight to shared memory
     int maxchild = 0;
@@ -1571,11 +1575,13 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
     int local_left = 0;  // local iterations still to run in this block
     for (; !init_err;) {
         const int par = it & 1;                     // parity of the iteration's inputs
-        // a local iteration reads this CTA's own counts (s_loc) and maps
+        // a local iteration reads this CTA's own counts (locS/P/F) and maps
         // item i to slot b * ch + i directly; a global one goes through the
         // prefix tables
-        const unsigned int nS = local ? s_loc[0] : s_pre[0][G], nP = local ? s_loc[1] : s_pre[1][G];
-        const unsigned int nF = it > 0 ? (local ? s_loc[2] : s_pre[2][G]) : 0u;
+        const unsigned int nS = local ? locS : s_pre[0][G], nP = local ? locP : s_pre[1][G];
+        const unsigned int nF = it > 0 ? (local ? locF : s_pre[2][G]) : 0u;
+        unsigned long long *const s_nsp = &s_nsp3[k3];
+        unsigned int *const s_nf = &s_nf3[k3];
         const unsigned long long pminb = s_c[1], smaxb = s_c[2];
         Slot &nxt = ctrl->slot[(it + 1) % NSLOT];
         // work distribution: every warp of the grid over all chunks, or (a
@@ -1622,7 +1628,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         }
         // fan candidates of this iteration go straight to the CTA's chunk
         auto fsink = [&](const FanEv &e) {
-            const unsigned int k = atomicAdd(&s_nf, 1u);
+            const unsigned int k = atomicAdd(s_nf, 1u);
             if (k < chF) fout[k] = e;
             else atomicExch(&ctrl->error, ERR_OVERFLOW);
         };
@@ -1638,7 +1644,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         auto put_direct = [&](const Win &c) {
             const bool sel = c.key <= tn;
             lsd.add(ST_STORED);
-            const unsigned long long old = atomicAdd(&s_nsp, sel ? 1ull : (1ull << 32));
+            const unsigned long long old = atomicAdd(s_nsp, sel ? 1ull : (1ull << 32));
             put_at(sel, sel ? (unsigned int)old : (unsigned int)(old >> 32), c);
             if (sel) atomicMax(&s_smax, (unsigned long long)__double_as_longlong(c.key));
             else atomicMin(&s_pmin, (unsigned long long)__double_as_longlong(c.key));
@@ -1802,7 +1808,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
                 if (hmax) atomicMax(&s_smax, ((unsigned long long)hmax << 32) | 0xffffffffull);
             }
             unsigned int sa, pa;
-            warp_chunk_alloc2(&s_nsp, ns_, np_, sa, pa);
+            warp_chunk_alloc2(s_nsp, ns_, np_, sa, pa);
             if (no > 0) put_at(s0, s0 ? sa++ : pa++, o0);
             if (no > 1) put_at(s1, s1 ? sa++ : pa++, o1);
             if (h2) put_at(s2, s2 ? sa : pa, o2);
@@ -1836,24 +1842,31 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             --local_left;
         }
         const bool next_local = local_left > 0;
+        // this iteration's totals (final after the publish barrier), read by
+        // every thread: the next iteration's own counts
+        const unsigned long long nsp_tot = *s_nsp;
+        const unsigned int nf_tot = *s_nf;
+        locS = min((unsigned int)nsp_tot, (unsigned int)ch);
+        locP = min((unsigned int)(nsp_tot >> 32), (unsigned int)ch);
+        locF = min(nf_tot, (unsigned int)chF);
         if (threadIdx.x == 0) {
             const int po = par ^ 1;  // parity of the next iteration's inputs
-            s_loc[0] = min((unsigned int)s_nsp, (unsigned int)ch);
-            s_loc[1] = min((unsigned int)(s_nsp >> 32), (unsigned int)ch);
-            s_loc[2] = min(s_nf, (unsigned int)chF);
-            p.ccnt[(size_t)(po * 3 + 0) * MAX_CTAS + b] = min((unsigned int)s_nsp, (unsigned int)ch);
-            p.ccnt[(size_t)(po * 3 + 1) * MAX_CTAS + b] = min((unsigned int)(s_nsp >> 32), (unsigned int)ch);
-            p.ccnt[(size_t)(par * 3 + 2) * MAX_CTAS + b] = min(s_nf, (unsigned int)chF);
+            p.ccnt[(size_t)(po * 3 + 0) * MAX_CTAS + b] = locS;
+            p.ccnt[(size_t)(po * 3 + 1) * MAX_CTAS + b] = locP;
+            p.ccnt[(size_t)(par * 3 + 2) * MAX_CTAS + b] = locF;
             // past half a chunk: finish this iteration, then grow the pool
             // and resume (host), instead of overflowing in a later one (a
             // CTA adds well under half a chunk per iteration)
             const unsigned long long soft = ch / 2, softF = chF / 2;
 #ifndef PCH_NO_SOFT
-            if ((s_nsp & 0xffffffffull) > soft || (s_nsp >> 32) > soft || s_nf > softF)
+            if ((nsp_tot & 0xffffffffull) > soft || (nsp_tot >> 32) > soft || nf_tot > softF)
                 atomicExch(&ctrl->grow, 1);
 #endif
-            s_nsp = 0ull;
-            s_nf = 0u;
+            // the copy of iteration i-1 (every thread read its totals
+            // before this iteration's publish barrier) serves iteration i+2
+            const int kp = k3 == 0 ? 2 : k3 - 1;
+            s_nsp3[kp] = 0ull;
+            s_nf3[kp] = 0u;
             if (!next_local) {  // the controller's extremes, over the local block
                 if (s_pmin != ~0ull) atomicMin(&nxt.pmin, s_pmin);
                 if (s_smax) atomicMax(&nxt.smax, s_smax);
@@ -1870,11 +1883,16 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             // after a global iteration the other CTAs may still be reading
             // this CTA's chunks (the distributed inputs): a grid barrier
             // before it writes its parity buffers again
+            // (local -> local: the publish barrier already ordered this
+            // CTA's outputs before the next iteration's loads, and the
+            // counters rotate)
             if (!local) {
                 grid_barrier<false>(ctrl, gen, [] {});
                 if (b == 0 && threadIdx.x == 0) s_st[ST_BARRIERS] += 1ull;
+            } else if (ROWS) {
+                __syncthreads();  // batched rows: measured faster with the CTA in step
             }
-            __syncthreads();  // s_loc and this CTA's outputs are visible to its warps
+            k3 = k3 == 2 ? 0 : k3 + 1;
             ++it;
             t = tn;
             local = true;
@@ -1896,6 +1914,7 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
             trr[TR_B1] = trr[TR_B_END] = trr[TR_B2] = globaltimer();
             trr[TR_NC] = (unsigned long long)ns + np;
         }
+        k3 = k3 == 2 ? 0 : k3 + 1;
         ++it;
         if (err || (ns == 0 && np == 0 && nf == 0)) break;
         t = tn;
@@ -1918,6 +1937,14 @@ __global__ void __launch_bounds__(TPB, PCH_LIVE_MIN_BLOCKS) pch_live(Params p) {
         ctrl->iterations = it;
         ctrl->t_final = t;
     }
+}
+
+// the instance for a solve: phase clocks only where requested; batched
+// rows and single fields separately tuned
+static const void *live_kernel(const Params &p) {
+    const bool rows = p.rows > 1;
+    if (p.phase) return rows ? (const void *)pch_live<true, true> : (const void *)pch_live<true, false>;
+    return rows ? (const void *)pch_live<false, true> : (const void *)pch_live<false, false>;
 }
 
 // ---------------------------------------------------------------------------
@@ -2361,7 +2388,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
         void *args[] = {&p};
         if (p.live)
         {
-            const void *kern = p.phase ? (const void *)pch_live<true> : (const void *)pch_live<false>;
+            const void *kern = live_kernel(p);
             CK(cudaLaunchCooperativeKernel(kern, dim3(p.live_grid), dim3(TPB), args, 0, st));
         }
         else
@@ -2394,7 +2421,7 @@ static int solve(pch_mesh *m, const int64_t *d_src, int nsrc, const pch_config *
             CK(cudaMemsetAsync(&p.ctrl->grow, 0, sizeof(int), st));
             CK(cudaMemsetAsync(&p.ctrl->bar_count, 0, sizeof(unsigned int), st));
             void *args2[] = {&p};
-            const void *kern = p.phase ? (const void *)pch_live<true> : (const void *)pch_live<false>;
+            const void *kern = live_kernel(p);
             CK(cudaLaunchCooperativeKernel(kern, dim3(p.live_grid), dim3(TPB), args2, 0, st));
             CK(cudaEventRecord(m->ev2, st));
             CK(cudaStreamSynchronize(st));
@@ -2744,7 +2771,7 @@ int pch_mesh_create(const int64_t *origin, const int64_t *opposite, const double
     cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device);
     m->clock_mhz = khz / 1000.0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_persistent, TPB, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live<true>, TPB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_live, pch_live<true, true>, TPB, 0);
     if (per_sm < 1 || per_sm_live < 1) return cleanup(PCH_ERR_CUDA, "persistent kernel cannot be resident");
     // persistent grids: every SM, as many co-resident CTAs as fit (<= 4)
     m->grid = nsm * std::min(per_sm, 4);
@@ -2782,7 +2809,7 @@ int pch_probe(int32_t device, double *out, int32_t n_out) {
     CK(cudaSetDevice(device));
     int nsm = 0, per_sm = 0;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_live<true>, TPB, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pch_live<true, true>, TPB, 0));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
